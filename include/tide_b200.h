@@ -1,0 +1,161 @@
+/*
+ * tide_b200.h — C ABI of the B200-native TIDE exit-decision hot path.
+ *
+ * Drop-in boundary for the reference's routing ops (earlyexit 0.1.0,
+ * /root/reference/pkg/src/earlyexit, "ee/" below) and for the four CUDA ops
+ * the paper registers as torch.ops.tide.* (PAPER.md:376-392, 413-419).
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer unless stated otherwise; the
+ *     caller allocates every output (the kernels never allocate global
+ *     memory).  `stream` is a cudaStream_t passed as void*.
+ *   - All calls are asynchronous and stream-ordered; none synchronises the
+ *     host.  Return value: TIDE_OK (0) or a negative TIDE_ERR_* code;
+ *     tide_last_error() returns the message of the calling thread's last
+ *     failure.
+ *   - dtype codes: TIDE_F32, TIDE_F16, TIDE_BF16.  Hidden rows are row-major
+ *     with a leading dimension `ld` in ELEMENTS.
+ *   - `workspace` is a TIDE_WORKSPACE_BYTES device buffer, zeroed once with
+ *     tide_workspace_init() and then reused by calls on ONE stream (it holds
+ *     the ordered look-back state of the stable compaction).
+ *   - There is no CPU fallback: unsupported shapes return
+ *     TIDE_ERR_UNSUPPORTED.
+ */
+#ifndef TIDE_B200_H_
+#define TIDE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TIDE_F32 0
+#define TIDE_F16 1
+#define TIDE_BF16 2
+
+#define TIDE_OK 0
+#define TIDE_ERR_ARG (-1)
+#define TIDE_ERR_UNSUPPORTED (-2)
+#define TIDE_ERR_CUDA (-3)
+#define TIDE_ERR_NODEVICE (-4)
+
+#define TIDE_MODE_PER_TOKEN 0       /* ee/runtime.py:28 */
+#define TIDE_MODE_BATCH_UNANIMOUS 1 /* ee/runtime.py:29 */
+#define TIDE_NO_EXIT (-1)           /* ee/runtime.py:35 */
+
+#define TIDE_WORKSPACE_BYTES (4u << 20)
+#define TIDE_MAX_LAYERS 256
+#define TIDE_MAX_DECODE_ROWS 16
+
+const char* tide_version(void);
+const char* tide_last_error(void);
+int tide_sm_count(int device);
+size_t tide_workspace_bytes(void);
+int tide_workspace_init(void* workspace, void* stream);
+
+/* 1 when (dtype, d, b) runs on the tcgen05 tensor-core kernel, else 0 (the
+ * CUDA-core kernel handles f32 and every other shape). */
+int tide_route_uses_tensor_cores(int32_t dtype, int32_t d, int32_t b);
+
+/*
+ * Fused RMSNorm + router + exit mask + stable compaction.
+ *
+ * Replaces, per checkpoint:
+ *   ee/router_ops.py:68-87    fused_layernorm_route(h, router, eps) -> scores
+ *   ee/runtime.py:149,171     mask = scores > np.float32(theta)
+ *   ee/router_ops.py:137-154  batch_compact(...).{exiting,continuing}_indices
+ *   ee/runtime.py:175-178     exited_at / exit_layers[exited_at] = k / remaining
+ *
+ * Rows routed: i in [0, n) — or [0, *n_dev) when n_dev != NULL (n is then the
+ * capacity, the device count was produced by a previous call's counts[1]).
+ * Row i reads h[row_idx[i]] when row_idx != NULL (peeling; rows_total bounds
+ * row_idx values), else h[i].
+ *   w_down  [b, d] row-major, dtype == h dtype (bf16/f16: tensor cores;
+ *           f32: CUDA cores).     w_up [b] f32.
+ * Outputs (each optional, NULL to skip), i = routed row:
+ *   scores[i] f32, logits[i] f32 (pre-sigmoid), mask[i] u8,
+ *   exit_idx[0..n_exit) / cont_idx[0..n-n_exit): stable partition, values are
+ *   i (ids_from_rows = 0) or row_idx[i] (ids_from_rows = 1),
+ *   exit_layers[row_idx ? row_idx[i] : i] = layer for exiting rows,
+ *   counts[0] = n_exit, counts[1] = n - n_exit.
+ */
+int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int64_t rows_total,
+               int32_t d, int32_t dtype, const int64_t* row_idx, const void* w_down,
+               const float* w_up, int32_t b, float eps, float theta, int64_t layer,
+               float* scores, float* logits, uint8_t* mask, int64_t* exit_idx,
+               int64_t* cont_idx, int32_t ids_from_rows, int64_t* exit_layers,
+               int64_t* counts, void* workspace, void* stream);
+
+/*
+ * Stable partition of a u8 mask (ee/router_ops.py:107-154, both strategies —
+ * they agree bitwise by contract).  Index outputs as tide_route; when `rows`
+ * != NULL also gathers rows (elem_bytes * d bytes each, leading dim ld_rows
+ * elements) into exit_rows [n_exit, d] / cont_rows [n - n_exit, d]
+ * (contiguous), which the caller sizes from a previous count.
+ */
+int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
+                 int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
+                 int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,
+                 void* cont_rows, int64_t* counts, void* workspace, void* stream);
+
+/*
+ * exit_scatter (ee/router_ops.py:170-176, normalize = 0) and exit_projection
+ * (ee/router_ops.py:179-188, normalize = 1):
+ *   out[positions[j]] = normalize ? rmsnorm(rows[src(j)], gain, eps) : rows[src(j)]
+ * src(j) = src_idx ? src_idx[j] : j.  out is f32 [*, d] with leading dim ld_out.
+ * gain may be NULL (no gain).  Positions are trusted (validated by caller).
+ */
+int tide_exit_project(const void* rows, int64_t ld_rows, int32_t dtype, const int64_t* src_idx,
+                      int64_t n_e, const int64_t* n_e_dev, int32_t d, const float* gain,
+                      float eps, int32_t normalize, const int64_t* positions, float* out,
+                      int64_t ld_out, void* stream);
+
+/*
+ * The output staging of posthoc_select (ee/runtime.py:176,180, ee/model.py:329-338):
+ *   out[i] = rmsnorm(H_{src(i)}[i], gain, eps), src(i) = exit_layers[i] + 1, or the
+ *   final capture (layer_ptrs[num_ptrs-1]) when exit_layers[i] == TIDE_NO_EXIT
+ *   (or exit_layers == NULL).  layer_ptrs is a HOST array of num_ptrs (= L+1)
+ *   device pointers, NULL allowed for layers never referenced.
+ */
+int tide_select_project(const void* const* layer_ptrs, int32_t num_ptrs, int64_t ld_h,
+                        int32_t dtype, const int64_t* exit_layers, int64_t n, int32_t d,
+                        const float* gain, float eps, float* out, int64_t ld_out, void* stream);
+
+/*
+ * Calibration labeller (ee/tensor_math.py:96-113, ee/calibration.py:201-219):
+ * one pass over the final rows and C checkpoint tensors (HOST array of C
+ * device pointers, same dtype / ld as final_h).  Per checkpoint c, row i:
+ *   sims[c*n+i] = clip(dot / (|h|*|f|), -1, 1), 0 for zero-norm rows;
+ *   labels_u8 / labels_f32 [c*n+i] = sims > f32(tau);
+ *   zero_mask[c*n+i] = 1 when either side has zero norm;
+ *   zero_counts[c] = #rows with a zero-norm side (int64; zeroed by the call).
+ * Any output may be NULL.
+ */
+int tide_cos_label(const void* const* ckpt_ptrs, int32_t C, const void* final_h, int64_t ld,
+                   int32_t dtype, int64_t n, int32_t d, float tau, float* sims,
+                   uint8_t* labels_u8, float* labels_f32, uint8_t* zero_mask,
+                   int64_t* zero_counts, void* stream);
+
+/*
+ * Decode-step router (n <= TIDE_MAX_DECODE_ROWS rows, every checkpoint in ONE
+ * launch) + exit resolution of posthoc_select (ee/runtime.py:151-178):
+ * per-token = first checkpoint >= k_min whose score > theta; batch-unanimous
+ * = first checkpoint where every row's score > theta.  Checkpoint c reads
+ * h_ptrs[c] [n, d] (ld_h) with router (w_ptrs[c] [b,d] dtype, wup_ptrs[c] [b]
+ * f32); HOST pointer arrays of length C, layers[c] ascending (host array).
+ * Outputs: scores/logits [C, n] f32, exit_layers [n] int64 (TIDE_NO_EXIT),
+ * exit_count[0] = rows that exited.
+ */
+int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n, int32_t d,
+                      int32_t dtype, const void* const* w_ptrs, const float* const* wup_ptrs,
+                      int32_t b, const int64_t* layers, float eps, float theta, int64_t k_min,
+                      int32_t mode, float* scores, float* logits, int64_t* exit_layers,
+                      int64_t* exit_count, void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TIDE_B200_H_ */

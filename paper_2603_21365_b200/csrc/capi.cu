@@ -1,0 +1,133 @@
+// C ABI entry points (include/tide_b200.h): argument checks, path selection
+// (tcgen05 vs CUDA-core), thread-local error reporting, device queries.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tide {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return TIDE_OK;
+}
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+}  // namespace tide
+
+using namespace tide;
+
+extern "C" {
+
+const char* tide_version(void) { return "tide_b200 0.1.0 (sm_100a)"; }
+
+const char* tide_last_error(void) { return g_err; }
+
+int tide_sm_count(int device) { return sm_count(device); }
+
+size_t tide_workspace_bytes(void) { return TIDE_WORKSPACE_BYTES; }
+
+int tide_workspace_init(void* workspace, void* stream) {
+  if (!workspace) return set_error(TIDE_ERR_ARG, "null workspace");
+  if (cudaMemsetAsync(workspace, 0, TIDE_WORKSPACE_BYTES, reinterpret_cast<cudaStream_t>(stream)) !=
+      cudaSuccess)
+    return set_error(TIDE_ERR_CUDA, "workspace memset failed");
+  return TIDE_OK;
+}
+
+int tide_route_uses_tensor_cores(int32_t dtype, int32_t d, int32_t b) {
+  return route_tc_supported(dtype, d, b) ? 1 : 0;
+}
+
+int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int64_t rows_total,
+               int32_t d, int32_t dtype, const int64_t* row_idx, const void* w_down,
+               const float* w_up, int32_t b, float eps, float theta, int64_t layer,
+               float* scores, float* logits, uint8_t* mask, int64_t* exit_idx,
+               int64_t* cont_idx, int32_t ids_from_rows, int64_t* exit_layers,
+               int64_t* counts, void* workspace, void* stream) {
+  if (d < 1 || b < 1 || n < 0) return set_error(TIDE_ERR_ARG, "tide_route: bad shape");
+  if (!w_down || !w_up || !workspace)
+    return set_error(TIDE_ERR_ARG, "tide_route: null weights or workspace");
+  if (n > 0 && !h) return set_error(TIDE_ERR_ARG, "tide_route: null hidden rows");
+  if (ld_h < d) return set_error(TIDE_ERR_ARG, "tide_route: ld_h < d");
+  if (dtype != TIDE_F32 && dtype != TIDE_F16 && dtype != TIDE_BF16)
+    return set_error(TIDE_ERR_ARG, "tide_route: bad dtype %d", dtype);
+  if (row_idx && rows_total < 1) return set_error(TIDE_ERR_ARG, "tide_route: rows_total required");
+  if (n == 0 && !n_dev) {
+    if (counts)
+      if (cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), reinterpret_cast<cudaStream_t>(stream)) !=
+          cudaSuccess)
+        return set_error(TIDE_ERR_CUDA, "memset counts failed");
+    return TIDE_OK;
+  }
+  RouteArgs a{};
+  a.h = h;
+  a.ld_h = ld_h;
+  a.n = n;
+  a.n_dev = n_dev;
+  a.rows_total = row_idx ? rows_total : n;
+  a.d = d;
+  a.dtype = dtype;
+  a.row_idx = row_idx;
+  a.w_down = w_down;
+  a.w_up = w_up;
+  a.b = b;
+  a.eps = eps;
+  a.theta = theta;
+  a.layer = layer;
+  a.scores = scores;
+  a.logits = logits;
+  a.mask = mask;
+  a.exit_idx = exit_idx;
+  a.cont_idx = cont_idx;
+  a.ids_from_rows = ids_from_rows;
+  a.exit_layers = exit_layers;
+  a.counts = counts;
+  a.workspace = workspace;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(h) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(w_down) & 15) == 0) && (ld_h % 8 == 0);
+  if (route_tc_supported(dtype, d, b) && aligned) return route_tc_launch(a, s);
+  return route_simt_launch(a, s);
+}
+
+int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
+                 int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
+                 int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,
+                 void* cont_rows, int64_t* counts, void* workspace, void* stream) {
+  if (n < 0 || (!mask && n > 0) || !workspace)
+    return set_error(TIDE_ERR_ARG, "tide_compact: bad arguments");
+  if (rows && (d < 1 || elem_bytes < 1 || ld_rows < d))
+    return set_error(TIDE_ERR_ARG, "tide_compact: bad row geometry");
+  return compact_launch(mask, n, n_dev, row_idx, ids_from_rows, rows, ld_rows, d, elem_bytes,
+                        exit_idx, cont_idx, exit_rows, cont_rows, counts, workspace,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

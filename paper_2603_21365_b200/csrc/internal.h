@@ -1,0 +1,49 @@
+// Host-side internals shared by the launchers and the C ABI (capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tide_b200.h"
+
+namespace tide {
+
+struct RouteArgs {
+  const void* h;
+  int64_t ld_h;
+  int64_t n;
+  const int64_t* n_dev;
+  int64_t rows_total;
+  int32_t d;
+  int32_t dtype;
+  const int64_t* row_idx;
+  const void* w_down;
+  const float* w_up;
+  int32_t b;
+  float eps;
+  float theta;
+  int64_t layer;
+  float* scores;
+  float* logits;
+  uint8_t* mask;
+  int64_t* exit_idx;
+  int64_t* cont_idx;
+  int32_t ids_from_rows;
+  int64_t* exit_layers;
+  int64_t* counts;
+  void* workspace;
+};
+
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+int sm_count(int device);
+
+bool route_tc_supported(int dtype, int d, int b);
+int route_tc_launch(const RouteArgs& a, cudaStream_t stream);
+int route_simt_launch(const RouteArgs& a, cudaStream_t stream);
+int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
+                   int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
+                   int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,
+                   void* cont_rows, int64_t* counts, void* workspace, cudaStream_t stream);
+
+}  // namespace tide

@@ -1,0 +1,186 @@
+// K3: exit scatter / exit projection and the posthoc output staging.
+//
+//   exit_scatter    ee/router_ops.py:170-176   out[pos] = rows
+//   exit_projection ee/router_ops.py:179-188   out[pos] = rmsnorm(rows, gain, eps)
+//   select_project  ee/runtime.py:176,180 + ee/model.py:329-338: every row is
+//                   final-normed from the layer it exits at (or the final
+//                   capture), producing the LM-head input in one pass.
+// rmsnorm follows ee/tensor_math.py:35-49 in f32: x / sqrt(sum(x^2)/d + eps) * gain.
+// One warp per row, 16-byte vector loads, the row held in registers between
+// the two passes when it fits (d <= 32 lanes x 8 x 4 elements).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tide {
+
+constexpr int kPThreads = 256;
+
+template <typename T>
+__device__ __forceinline__ void norm_row(const T* __restrict__ src, float* __restrict__ dst, int d,
+                                         const float* __restrict__ gain, float eps,
+                                         int normalize) {
+  const int lane = threadIdx.x & 31;
+  constexpr int V = 16 / sizeof(T);
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (d % V == 0);
+  float ss = 0.f;
+  if (normalize) {
+    if (vec) {
+      for (int k = lane * V; k < d; k += 32 * V) {
+        float f[V];
+        unpack16(*reinterpret_cast<const uint4*>(src + k), f, (const T*)nullptr);
+#pragma unroll
+        for (int e = 0; e < V; ++e) ss = fmaf(f[e], f[e], ss);
+      }
+    } else {
+      for (int k = lane; k < d; k += 32) {
+        const float x = to_f32<T>(src[k]);
+        ss = fmaf(x, x, ss);
+      }
+    }
+    ss = warp_sum_f32(ss);
+  }
+  const float den = normalize ? __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps)) : 1.0f;
+  if (vec) {
+    for (int k = lane * V; k < d; k += 32 * V) {
+      float f[V];
+      unpack16(*reinterpret_cast<const uint4*>(src + k), f, (const T*)nullptr);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        float y = normalize ? __fdiv_rn(f[e], den) : f[e];
+        if (normalize && gain) y = __fmul_rn(y, gain[k + e]);
+        f[e] = y;
+      }
+#pragma unroll
+      for (int e = 0; e < V; e += 4)
+        *reinterpret_cast<float4*>(dst + k + e) = make_float4(f[e], f[e + 1], f[e + 2], f[e + 3]);
+    }
+  } else {
+    for (int k = lane; k < d; k += 32) {
+      float y = to_f32<T>(src[k]);
+      if (normalize) {
+        y = __fdiv_rn(y, den);
+        if (gain) y = __fmul_rn(y, gain[k]);
+      }
+      dst[k] = y;
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kPThreads)
+    exit_project_kernel(const T* rows, int64_t ld_rows, const int64_t* src_idx, int64_t n_e_host,
+                        const int64_t* n_e_dev, int d, const float* gain, float eps, int normalize,
+                        const int64_t* positions, float* out, int64_t ld_out) {
+  const int64_t n_e = n_e_dev ? *n_e_dev : n_e_host;
+  const int64_t warps = (int64_t)gridDim.x * (kPThreads / 32);
+  for (int64_t j = (int64_t)blockIdx.x * (kPThreads / 32) + (threadIdx.x >> 5); j < n_e;
+       j += warps) {
+    const int64_t s = src_idx ? src_idx[j] : j;
+    norm_row<T>(rows + s * ld_rows, out + positions[j] * ld_out, d, gain, eps, normalize);
+  }
+}
+
+constexpr int kMaxPtrs = TIDE_MAX_LAYERS + 1;
+struct SelectParams {
+  const void* layer[kMaxPtrs];
+  int32_t num;
+  int64_t ld_h, n, ld_out;
+  int32_t d;
+  const int64_t* exit_layers;
+  const float* gain;
+  float eps;
+  float* out;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kPThreads) select_project_kernel(const __grid_constant__ SelectParams p) {
+  const int64_t warps = (int64_t)gridDim.x * (kPThreads / 32);
+  for (int64_t i = (int64_t)blockIdx.x * (kPThreads / 32) + (threadIdx.x >> 5); i < p.n;
+       i += warps) {
+    int64_t src = p.num - 1;
+    if (p.exit_layers) {
+      const int64_t k = p.exit_layers[i];
+      if (k != TIDE_NO_EXIT && k + 1 >= 0 && k + 1 < p.num) src = k + 1;
+    }
+    const T* row = reinterpret_cast<const T*>(p.layer[src]) + i * p.ld_h;
+    norm_row<T>(row, p.out + i * p.ld_out, p.d, p.gain, p.eps, 1);
+  }
+}
+
+static int grid_for(int64_t rows) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int64_t blocks = (rows + (kPThreads / 32) - 1) / (kPThreads / 32);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count(dev) * 8));
+}
+
+}  // namespace tide
+
+using namespace tide;
+
+extern "C" int tide_exit_project(const void* rows, int64_t ld_rows, int32_t dtype,
+                                 const int64_t* src_idx, int64_t n_e, const int64_t* n_e_dev,
+                                 int32_t d, const float* gain, float eps, int32_t normalize,
+                                 const int64_t* positions, float* out, int64_t ld_out,
+                                 void* stream) {
+  if (d < 1 || n_e < 0 || !out || !positions || (!rows && n_e > 0))
+    return set_error(TIDE_ERR_ARG, "tide_exit_project: bad arguments");
+  if (n_e == 0 && !n_e_dev) return TIDE_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = grid_for(std::max<int64_t>(n_e, 1));
+  switch (dtype) {
+    case TIDE_F32:
+      exit_project_kernel<float><<<grid, kPThreads, 0, s>>>((const float*)rows, ld_rows, src_idx,
+                                                            n_e, n_e_dev, d, gain, eps, normalize,
+                                                            positions, out, ld_out);
+      break;
+    case TIDE_BF16:
+      exit_project_kernel<__nv_bfloat16><<<grid, kPThreads, 0, s>>>(
+          (const __nv_bfloat16*)rows, ld_rows, src_idx, n_e, n_e_dev, d, gain, eps, normalize,
+          positions, out, ld_out);
+      break;
+    case TIDE_F16:
+      exit_project_kernel<__half><<<grid, kPThreads, 0, s>>>((const __half*)rows, ld_rows, src_idx,
+                                                             n_e, n_e_dev, d, gain, eps, normalize,
+                                                             positions, out, ld_out);
+      break;
+    default:
+      return set_error(TIDE_ERR_ARG, "bad dtype %d", dtype);
+  }
+  return check_launch("exit_project_kernel");
+}
+
+extern "C" int tide_select_project(const void* const* layer_ptrs, int32_t num_ptrs, int64_t ld_h,
+                                   int32_t dtype, const int64_t* exit_layers, int64_t n,
+                                   int32_t d, const float* gain, float eps, float* out,
+                                   int64_t ld_out, void* stream) {
+  if (num_ptrs < 1 || num_ptrs > kMaxPtrs || d < 1 || n < 0 || !out || !layer_ptrs ||
+      !layer_ptrs[num_ptrs - 1])
+    return set_error(TIDE_ERR_ARG, "tide_select_project: bad arguments");
+  if (n == 0) return TIDE_OK;
+  SelectParams p{};
+  for (int i = 0; i < num_ptrs; ++i) p.layer[i] = layer_ptrs[i];
+  p.num = num_ptrs;
+  p.ld_h = ld_h;
+  p.n = n;
+  p.ld_out = ld_out;
+  p.d = d;
+  p.exit_layers = exit_layers;
+  p.gain = gain;
+  p.eps = eps;
+  p.out = out;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = grid_for(n);
+  switch (dtype) {
+    case TIDE_F32: select_project_kernel<float><<<grid, kPThreads, 0, s>>>(p); break;
+    case TIDE_BF16: select_project_kernel<__nv_bfloat16><<<grid, kPThreads, 0, s>>>(p); break;
+    case TIDE_F16: select_project_kernel<__half><<<grid, kPThreads, 0, s>>>(p); break;
+    default: return set_error(TIDE_ERR_ARG, "bad dtype %d", dtype);
+  }
+  return check_launch("select_project_kernel");
+}

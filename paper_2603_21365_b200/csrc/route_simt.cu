@@ -1,0 +1,416 @@
+// CUDA-core router kernels.
+//
+// route_simt_kernel  — fused_layernorm_route + mask + stable compaction for
+//   shapes the tensor-core kernel does not take (f32 rows: the reference's
+//   own dtype, where 1e-5 logit parity needs f32 products; b > 256; d % 8).
+//   16 rows x 128 bottleneck columns per pass, K staged through smem in
+//   chunks of 32, 2x4 register micro-tile per thread, f32 accumulation.
+// route_decode_kernel — the decode step (n <= 16 rows) for EVERY checkpoint
+//   in one launch: grid (checkpoint, K-split); partial pre-activations are
+//   reduced in a fixed order by the last CTA of each checkpoint (deterministic),
+//   and the last checkpoint to finish resolves the exit per row
+//   (ee/runtime.py:151-178).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tide {
+
+constexpr int kSR = 16;    // rows per CTA
+constexpr int kSJ = 128;   // bottleneck columns per pass
+constexpr int kSK = 32;    // K chunk
+constexpr int kSThreads = 256;
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p) {
+  return to_f32<T>(*p);
+}
+
+// acc[r2][c4] += sum_k X[ty + 8 r2][k] * W[j0 + tx + 32 c4][k] over k in [k0, k1)
+// Also accumulates sum of squares of the 16 rows into ss_s[16] (if non-null).
+template <typename XT>
+__device__ __forceinline__ void gemm_16x128(const XT* const* xrow, const XT* W, int64_t ldw,
+                                            int j0, int b, int64_t k0, int64_t k1,
+                                            float (&acc)[2][4], float (*Xs)[kSK + 1],
+                                            float (*Ws)[kSK + 1], float* ss_s) {
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  for (int64_t kc = k0; kc < k1; kc += kSK) {
+    // stage X chunk [16][32]
+    for (int e = tid; e < kSR * kSK; e += kSThreads) {
+      const int r = e / kSK, kk = e % kSK;
+      const int64_t k = kc + kk;
+      float v = 0.f;
+      if (xrow[r] && k < k1) v = ldf(xrow[r] + k);
+      Xs[r][kk] = v;
+    }
+    // stage W chunk [128][32]
+    for (int e = tid; e < kSJ * kSK; e += kSThreads) {
+      const int j = e / kSK, kk = e % kSK;
+      const int64_t k = kc + kk;
+      float v = 0.f;
+      if (j0 + j < b && k < k1) v = ldf(W + (int64_t)(j0 + j) * ldw + k);
+      Ws[j][kk] = v;
+    }
+    __syncthreads();
+    if (ss_s && j0 == 0 && tid < kSR * 8) {
+      // 8 threads per row reduce 4 elements each, then shuffle within the 8
+      const int r = tid >> 3, part = tid & 7;
+      float s = 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float x = Xs[r][part * 4 + u];
+        s = fmaf(x, x, s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (part == 0) ss_s[r] += s;
+    }
+#pragma unroll 8
+    for (int kk = 0; kk < kSK; ++kk) {
+      const float x0 = Xs[ty][kk], x1 = Xs[ty + 8][kk];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float w = Ws[tx + 32 * c][kk];
+        acc[0][c] = fmaf(x0, w, acc[0][c]);
+        acc[1][c] = fmaf(x1, w, acc[1][c]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct SimtParams {
+  int64_t n_host;
+  const int64_t* n_dev;
+  int32_t d, b;
+  int64_t ld_h;
+  const void* h;
+  const int64_t* row_idx;
+  int32_t ids_from_rows;
+  const void* w_down;
+  const float* w_up;
+  float eps, inv_d, theta;
+  int64_t layer;
+  float* scores;
+  float* logits;
+  uint8_t* mask;
+  int64_t* exit_idx;
+  int64_t* cont_idx;
+  int64_t* exit_layers;
+  int64_t* counts;
+  Workspace* ws;
+};
+
+template <typename XT>
+__global__ void __launch_bounds__(kSThreads) route_simt_kernel(const SimtParams p) {
+  __shared__ float Xs[kSR][kSK + 1];
+  __shared__ float Ws[kSJ][kSK + 1];
+  __shared__ float ss_s[kSR];
+  __shared__ float t_s[kSR];
+  __shared__ const XT* xrow[kSR];
+  __shared__ uint32_t bits_s;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
+  const uint32_t tag = launch_tag(p.ws);
+  const int64_t nblk = (n + kSR - 1) / kSR;
+  const XT* h = reinterpret_cast<const XT*>(p.h);
+  const XT* W = reinterpret_cast<const XT*>(p.w_down);
+  const bool gathered = p.row_idx != nullptr;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t r0 = blk * kSR;
+    if (tid < kSR) {
+      const int64_t r = r0 + tid;
+      xrow[tid] = r < n ? h + (gathered ? p.row_idx[r] : r) * p.ld_h : nullptr;
+      ss_s[tid] = 0.f;
+      t_s[tid] = 0.f;
+    }
+    __syncthreads();
+    for (int j0 = 0; j0 < p.b; j0 += kSJ) {
+      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      gemm_16x128<XT>(xrow, W, p.d, j0, p.b, 0, p.d, acc, Xs, Ws, ss_s);
+      // all of ss_s is final after the first pass (j0 == 0) completed
+#pragma unroll
+      for (int r2 = 0; r2 < 2; ++r2) {
+        const int r = ty + 8 * r2;
+        const float scale = rms_scale(ss_s[r], p.inv_d, p.eps);
+        float part = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int j = j0 + tx + 32 * c;
+          if (j < p.b) part = fmaf(p.w_up[j], silu_f32(__fmul_rn(acc[r2][c], scale)), part);
+        }
+        part = warp_sum_f32(part);
+        if (tx == 0) t_s[r] += part;
+      }
+      __syncthreads();
+    }
+    // finalize rows (warp 0), ballot the exit bits
+    if (ty == 0) {
+      const int64_t r = r0 + tx;
+      bool ex = false;
+      if (tx < kSR && r < n) {
+        const float t = t_s[tx];
+        const float score = score_from_logit(t);
+        ex = score > p.theta;
+        if (p.scores) p.scores[r] = score;
+        if (p.logits) p.logits[r] = t;
+        if (p.mask) p.mask[r] = ex ? 1 : 0;
+        if (ex && p.exit_layers) p.exit_layers[gathered ? p.row_idx[r] : r] = p.layer;
+      }
+      const uint32_t bits = __ballot_sync(0xffffffffu, ex);
+      if (p.exit_idx || p.cont_idx || p.counts) {
+        const uint32_t agg = __popc(bits);
+        const uint32_t E = lookback_exclusive(p.ws->status, tag, blk, agg);
+        if (tx < kSR && r < n) {
+          const int64_t rank = (int64_t)E + __popc(bits & ((1u << tx) - 1u));
+          const int64_t id = (p.ids_from_rows && gathered) ? p.row_idx[r] : r;
+          if (ex) {
+            if (p.exit_idx) p.exit_idx[rank] = id;
+          } else if (p.cont_idx) {
+            p.cont_idx[r - rank] = id;
+          }
+        }
+        if (blk == nblk - 1 && tx == 0 && p.counts) {
+          p.counts[0] = (int64_t)E + agg;
+          p.counts[1] = n - ((int64_t)E + agg);
+        }
+      }
+      (void)bits_s;
+    }
+    __syncthreads();
+  }
+  if (nblk == 0 && blockIdx.x == 0 && tid == 0 && p.counts) {
+    p.counts[0] = 0;
+    p.counts[1] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) launch_done(p.ws);
+}
+
+int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
+  if (a.b < 1 || a.d < 1) return set_error(TIDE_ERR_ARG, "empty router");
+  SimtParams p{};
+  p.n_host = a.n;
+  p.n_dev = a.n_dev;
+  p.d = a.d;
+  p.b = a.b;
+  p.ld_h = a.ld_h;
+  p.h = a.h;
+  p.row_idx = a.row_idx;
+  p.ids_from_rows = a.ids_from_rows;
+  p.w_down = a.w_down;
+  p.w_up = a.w_up;
+  p.eps = a.eps;
+  p.inv_d = (float)(1.0 / (double)a.d);
+  p.theta = a.theta;
+  p.layer = a.layer;
+  p.scores = a.scores;
+  p.logits = a.logits;
+  p.mask = a.mask;
+  p.exit_idx = a.exit_idx;
+  p.cont_idx = a.cont_idx;
+  p.exit_layers = a.exit_layers;
+  p.counts = a.counts;
+  p.ws = reinterpret_cast<Workspace*>(a.workspace);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int64_t nblk = (a.n + kSR - 1) / kSR;
+  if (nblk > kMaxParts) return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)sm_count(dev) * 8));
+  switch (a.dtype) {
+    case TIDE_F32: route_simt_kernel<float><<<grid, kSThreads, 0, stream>>>(p); break;
+    case TIDE_BF16: route_simt_kernel<__nv_bfloat16><<<grid, kSThreads, 0, stream>>>(p); break;
+    case TIDE_F16: route_simt_kernel<__half><<<grid, kSThreads, 0, stream>>>(p); break;
+    default: return set_error(TIDE_ERR_ARG, "bad dtype %d", a.dtype);
+  }
+  return check_launch("route_simt_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// decode: all checkpoints, n <= 16 rows, one launch
+// ---------------------------------------------------------------------------
+constexpr int kMaxDecodeC = kMaxTickets;
+struct DecodeParams {
+  const void* h[kMaxDecodeC];
+  const void* w[kMaxDecodeC];
+  const float* wup[kMaxDecodeC];
+  int64_t layers[kMaxDecodeC];
+  int32_t C, d, b, ks;
+  int64_t ld_h, n, k_min;
+  int32_t mode;
+  float eps, inv_d, theta;
+  float* scores;
+  float* logits;
+  int64_t* exit_layers;
+  int64_t* exit_count;
+  Workspace* ws;
+};
+
+template <typename XT>
+__global__ void __launch_bounds__(kSThreads) route_decode_kernel(const DecodeParams p) {
+  __shared__ float Xs[kSR][kSK + 1];
+  __shared__ float Ws[kSJ][kSK + 1];
+  __shared__ float ss_s[kSR];
+  __shared__ const XT* xrow[kSR];
+  __shared__ unsigned int last_s;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int c = blockIdx.x, ks = blockIdx.y;
+  const int bstride = p.b;                       // floats per row of partial a
+  const int per_ks = kSR * bstride + kSR;        // partial a + partial sumsq
+  float* part = p.ws->partials + ((int64_t)c * p.ks + ks) * per_ks;
+  const int64_t kchunk = ((p.d + p.ks - 1) / p.ks + kSK - 1) / kSK * kSK;
+  const int64_t k0 = std::min<int64_t>((int64_t)ks * kchunk, p.d);
+  const int64_t k1 = std::min<int64_t>(k0 + kchunk, p.d);
+  const XT* h = reinterpret_cast<const XT*>(p.h[c]);
+  const XT* W = reinterpret_cast<const XT*>(p.w[c]);
+  if (tid < kSR) {
+    xrow[tid] = tid < p.n ? h + tid * p.ld_h : nullptr;
+    ss_s[tid] = 0.f;
+  }
+  __syncthreads();
+  for (int j0 = 0; j0 < p.b; j0 += kSJ) {
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    gemm_16x128<XT>(xrow, W, p.d, j0, p.b, k0, k1, acc, Xs, Ws, ss_s);
+#pragma unroll
+    for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int j = j0 + tx + 32 * cc;
+        if (j < p.b) part[(ty + 8 * r2) * bstride + j] = acc[r2][cc];
+      }
+  }
+  __syncthreads();
+  if (tid < kSR) part[kSR * bstride + tid] = ss_s[tid];
+  // ticket: the last K-split CTA of checkpoint c reduces in fixed order
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned int prev = atomicAdd(&p.ws->tickets[c], 1u);
+    last_s = (prev == (unsigned int)(p.ks - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (last_s) {
+    __threadfence();
+    float* base = p.ws->partials + (int64_t)c * p.ks * per_ks;
+    if (tid < kSR) {
+      float s = 0.f;
+      for (int q = 0; q < p.ks; ++q) s += base[(int64_t)q * per_ks + kSR * bstride + tid];
+      ss_s[tid] = s;
+    }
+    __syncthreads();
+    // warp ty owns rows ty, ty+8; lanes stride the bottleneck
+    for (int r2 = 0; r2 < 2; ++r2) {
+      const int r = ty + 8 * r2;
+      const float scale = rms_scale(ss_s[r], p.inv_d, p.eps);
+      float t = 0.f;
+      for (int j = tx; j < p.b; j += 32) {
+        float a = 0.f;
+        for (int q = 0; q < p.ks; ++q) a += base[(int64_t)q * per_ks + r * bstride + j];
+        t = fmaf(p.wup[c][j], silu_f32(__fmul_rn(a, scale)), t);
+      }
+      t = warp_sum_f32(t);
+      if (tx == 0 && r < p.n) {
+        if (p.scores) p.scores[(int64_t)c * p.n + r] = score_from_logit(t);
+        if (p.logits) p.logits[(int64_t)c * p.n + r] = t;
+        p.ws->dec_scores[c * kSR + r] = score_from_logit(t);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.ws->tickets[c] = 0;  // reset this checkpoint's ticket for the next launch
+      __threadfence();
+      const unsigned int prev = atomicAdd(&p.ws->ticket, 1u);
+      last_s = (prev == (unsigned int)(p.C - 1)) ? 2u : 0u;
+    }
+    __syncthreads();
+    if (last_s == 2u) {
+      __threadfence();
+      // exit resolution, rows in lanes of warp 0
+      if (ty == 0) {
+        const int r = tx;
+        int64_t exit_layer = TIDE_NO_EXIT;
+        if (p.mode == TIDE_MODE_PER_TOKEN) {
+          for (int cc = 0; cc < p.C && r < p.n; ++cc) {
+            if (p.layers[cc] < p.k_min) continue;
+            const float s = p.ws->dec_scores[cc * kSR + r];
+            if (s > p.theta) { exit_layer = p.layers[cc]; break; }
+          }
+        } else {
+          for (int cc = 0; cc < p.C; ++cc) {
+            if (p.layers[cc] < p.k_min) continue;
+            const bool fire =
+                r >= p.n || p.ws->dec_scores[cc * kSR + r] > p.theta;
+            if (__all_sync(0xffffffffu, fire)) { exit_layer = p.layers[cc]; break; }
+          }
+        }
+        if (r < p.n && p.exit_layers) p.exit_layers[r] = exit_layer;
+        const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, r < p.n && exit_layer != TIDE_NO_EXIT));
+        if (tx == 0) {
+          if (p.exit_count) p.exit_count[0] = cnt;
+          p.ws->ticket = 0;
+        }
+      }
+    }
+  }
+}
+
+int route_decode_launch(const DecodeParams& p0, int dtype, cudaStream_t stream) {
+  DecodeParams p = p0;
+  const int64_t per_ks = (int64_t)kSR * p.b + kSR;
+  int ks = std::max(1, std::min<int>((p.d + 255) / 256, 148 / std::max(1, p.C)));
+  while (ks > 1 && (int64_t)p.C * ks * per_ks > kMaxPartials) --ks;
+  if ((int64_t)p.C * ks * per_ks > kMaxPartials)
+    return set_error(TIDE_ERR_UNSUPPORTED, "decode problem too large for workspace");
+  p.ks = ks;
+  dim3 grid(p.C, ks);
+  switch (dtype) {
+    case TIDE_F32: route_decode_kernel<float><<<grid, kSThreads, 0, stream>>>(p); break;
+    case TIDE_BF16: route_decode_kernel<__nv_bfloat16><<<grid, kSThreads, 0, stream>>>(p); break;
+    case TIDE_F16: route_decode_kernel<__half><<<grid, kSThreads, 0, stream>>>(p); break;
+    default: return set_error(TIDE_ERR_ARG, "bad dtype %d", dtype);
+  }
+  return check_launch("route_decode_kernel");
+}
+
+}  // namespace tide
+
+extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n,
+                                 int32_t d, int32_t dtype, const void* const* w_ptrs,
+                                 const float* const* wup_ptrs, int32_t b, const int64_t* layers,
+                                 float eps, float theta, int64_t k_min, int32_t mode,
+                                 float* scores, float* logits, int64_t* exit_layers,
+                                 int64_t* exit_count, void* workspace, void* stream) {
+  using namespace tide;
+  if (C < 1 || C > kMaxDecodeC) return set_error(TIDE_ERR_ARG, "C must be in [1, %d]", kMaxDecodeC);
+  if (n < 1 || n > kSR) return set_error(TIDE_ERR_ARG, "decode rows must be in [1, %d]", kSR);
+  if (d < 1 || b < 1) return set_error(TIDE_ERR_ARG, "bad shape");
+  if (!workspace) return set_error(TIDE_ERR_ARG, "workspace required");
+  DecodeParams p{};
+  for (int c = 0; c < C; ++c) {
+    p.h[c] = h_ptrs[c];
+    p.w[c] = w_ptrs[c];
+    p.wup[c] = wup_ptrs[c];
+    p.layers[c] = layers[c];
+  }
+  p.C = C;
+  p.d = d;
+  p.b = b;
+  p.ld_h = ld_h;
+  p.n = n;
+  p.k_min = k_min;
+  p.mode = mode;
+  p.eps = eps;
+  p.inv_d = (float)(1.0 / (double)d);
+  p.theta = theta;
+  p.scores = scores;
+  p.logits = logits;
+  p.exit_layers = exit_layers;
+  p.exit_count = exit_count;
+  p.ws = reinterpret_cast<Workspace*>(workspace);
+  return route_decode_launch(p, dtype, reinterpret_cast<cudaStream_t>(stream));
+}

@@ -1,0 +1,488 @@
+// K1 (+K2 fused): fused RMSNorm + router + exit mask + stable compaction on
+// tcgen05 tensor cores.
+//
+// Restates, for a block of rows at once:
+//   ee/router_ops.py:68-87   fused_layernorm_route  (score per row)
+//   ee/runtime.py:149,171    mask = score > f32(theta)       (strict)
+//   ee/router_ops.py:116-134 _compact_prefix_sum    (stable partition indices)
+//   ee/runtime.py:175-178    exited_at / exit_layers / remaining (row_idx mode)
+//
+// Layout: h [rows, d] (bf16 | f16) row-major, W_down [b, d] same dtype
+// (K-major for the MMA), w_up [b] f32.  Accumulator D = h_tile . W^T lives in
+// TMEM (128 lanes = 128 tokens, N = b columns, f32).
+//
+// CTA roles (224 threads, one CTA per SM, persistent over row groups):
+//   warp 0      TMA producer: W k-chunk into the W ring, then one A k-chunk
+//               per tile into the A ring (128-row box, 32-row boxes for the
+//               ragged tail, or tile::gather4 rows when peeling by row_idx).
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer.  K-outer /
+//               M-inner: each W k-chunk in smem feeds up to 4 token tiles,
+//               whose accumulators all live in TMEM at once (4 x 128 cols),
+//               so W is re-read from L2 once per 512 tokens, not per 128.
+//   warps 2-5   sum-of-squares of every A slot from smem while the MMAs run
+//               (RMS statistics fused into the stream), then the epilogue:
+//               tcgen05.ld the row's b accumulators, scale, SiLU, dot w_up,
+//               f64 sigmoid, strict threshold, ballot the exit bits.
+//   warp 6      compaction: per-group popc scan + ordered decoupled look-back
+//               across groups, writes int64 exit / continuing indices.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tide {
+
+constexpr int kThreadsTC = 224;
+constexpr int kMaxNA = 16;
+constexpr int kMaxNW = 4;
+constexpr int kASlotBytes = 128 * 128;  // 128 rows x 64 cols x 2 B
+
+struct TcParams {
+  int64_t n_host;
+  const int64_t* n_dev;
+  int64_t rows_total;
+  int32_t d, b, npad, bp, tpg, nk, na, nw;
+  uint32_t idesc, tmem_cols, wslot;
+  uint32_t off_a, off_wup, off_bar, off_words, off_ids, off_tmem;
+  const int64_t* row_idx;
+  int32_t ids_from_rows;
+  const float* w_up;
+  float eps, inv_d, theta;
+  int64_t layer;
+  float* scores;
+  float* logits;
+  uint8_t* mask;
+  int64_t* exit_idx;
+  int64_t* cont_idx;
+  int64_t* exit_layers;
+  int64_t* counts;
+  Workspace* ws;
+};
+
+__device__ __forceinline__ void group_range(int64_t g, int64_t n, int64_t n32, int64_t ng,
+                                            int64_t& r0, int64_t& r1) {
+  r0 = (g * n32 / ng) * 32;
+  r1 = ((g + 1) * n32 / ng) * 32;
+  if (r1 > n) r1 = n;
+}
+
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    route_tc_kernel(const __grid_constant__ CUtensorMap tm_h128,
+                    const __grid_constant__ CUtensorMap tm_h32,
+                    const __grid_constant__ CUtensorMap tm_w,
+                    const __grid_constant__ CUtensorMap tm_g4, const __grid_constant__ TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sW = smem;
+  uint8_t* sA = smem + p.off_a;
+  float* sWup = reinterpret_cast<float*>(smem + p.off_wup);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* w_full = bars;
+  uint64_t* w_empty = bars + kMaxNW;
+  uint64_t* a_full = bars + 2 * kMaxNW;
+  uint64_t* a_empty = a_full + kMaxNA;
+  uint64_t* t_full = a_empty + kMaxNA;
+  uint64_t* t_empty = t_full + 4;
+  uint64_t* m_full = t_empty + 4;
+  uint64_t* m_empty = m_full + 2;
+  uint32_t* words = reinterpret_cast<uint32_t*>(smem + p.off_words);
+  uint32_t* ids = reinterpret_cast<uint32_t*>(smem + p.off_ids);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.off_tmem);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
+  const int64_t n32 = (n + 31) / 32;
+  const int64_t G = gridDim.x;
+  const int64_t cpg = (int64_t)p.tpg * 4;
+  int64_t NG = n32 < G ? n32 : G;
+  if ((n32 + cpg - 1) / cpg > NG) NG = (n32 + cpg - 1) / cpg;
+  const uint32_t tag = launch_tag(p.ws);
+  const bool gathered = p.row_idx != nullptr;
+  const bool need_scan = p.exit_idx || p.cont_idx || p.counts;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_w);
+    prefetch_tmap(gathered ? &tm_g4 : &tm_h128);
+    if (!gathered) prefetch_tmap(&tm_h32);
+    for (int i = 0; i < p.nw; ++i) {
+      mbar_init(&w_full[i], 1);
+      mbar_init(&w_empty[i], 1);
+    }
+    for (int i = 0; i < p.na; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1 + 4);  // MMA commit + 4 sum-of-squares warps
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&m_full[i], 4);
+      mbar_init(&m_empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, p.tmem_cols);
+    tmem_relinquish();
+  }
+  for (int i = threadIdx.x; i < p.b; i += blockDim.x) sWup[i] = p.w_up[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ----------------------------------------------------------- producer
+    const uint64_t pol_h = policy_evict_first();
+    const uint64_t pol_w = policy_evict_last();
+    int as = 0, aph = 0, wsl = 0, wph = 0;
+    for (int64_t g = blockIdx.x; g < NG; g += G) {
+      int64_t r0, r1;
+      group_range(g, n, n32, NG, r0, r1);
+      const int T = (int)((r1 - r0 + 127) / 128);
+      if (gathered) {
+        __syncwarp();
+        for (int64_t i = r0 + lane; i < r0 + (int64_t)T * 128; i += 32)
+          ids[i - r0] = i < r1 ? (uint32_t)p.row_idx[i] : (uint32_t)p.rows_total;
+        __syncwarp();
+      }
+      if (lane == 0) {
+        for (int kc = 0; kc < p.nk; ++kc) {
+          mbar_wait(&w_empty[wsl], wph ^ 1);
+          mbar_arrive_expect_tx(&w_full[wsl], p.wslot);
+          tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
+          if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
+          for (int t = 0; t < T; ++t) {
+            mbar_wait(&a_empty[as], aph ^ 1);
+            uint8_t* dst = sA + (size_t)as * kASlotBytes;
+            const int64_t rb = r0 + (int64_t)t * 128;
+            const int rows_in = (int)((r1 - rb) < 128 ? (r1 - rb) : 128);
+            if (!gathered) {
+              if (rows_in == 128) {
+                mbar_arrive_expect_tx(&a_full[as], kASlotBytes);
+                tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
+              } else {
+                const int nb = (rows_in + 31) / 32;
+                mbar_arrive_expect_tx(&a_full[as], nb * 4096);
+                for (int s = 0; s < nb; ++s)
+                  tma_load_2d(dst + s * 4096, &tm_h32, &a_full[as], kc * 64, (int)(rb + 32 * s),
+                              pol_h);
+              }
+            } else {
+              const int ng4 = (rows_in + 3) / 4;
+              mbar_arrive_expect_tx(&a_full[as], ng4 * 512);
+              const uint32_t* id = ids + t * 128;
+              for (int q = 0; q < ng4; ++q)
+                tma_gather4(dst + q * 512, &tm_g4, &a_full[as], kc * 64, (int)id[4 * q],
+                            (int)id[4 * q + 1], (int)id[4 * q + 2], (int)id[4 * q + 3], pol_h);
+            }
+            if (++as == p.na) { as = 0; aph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ----------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int as = 0, aph = 0, wsl = 0, wph = 0;
+      uint32_t accph = 0;
+      for (int64_t g = blockIdx.x; g < NG; g += G) {
+        int64_t r0, r1;
+        group_range(g, n, n32, NG, r0, r1);
+        const int T = (int)((r1 - r0 + 127) / 128);
+        for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
+        tc_fence_after();
+        for (int kc = 0; kc < p.nk; ++kc) {
+          mbar_wait(&w_full[wsl], wph);
+          tc_fence_after();
+          const uint32_t wbase = smem_u32(sW + (size_t)wsl * p.wslot);
+          for (int t = 0; t < T; ++t) {
+            mbar_wait(&a_full[as], aph);
+            tc_fence_after();
+            const uint32_t abase = smem_u32(sA + (size_t)as * kASlotBytes);
+            const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(dt, sw128_kmajor_desc(abase + 32 * k), sw128_kmajor_desc(wbase + 32 * k),
+                         p.idesc, (kc | k) != 0);
+            tc_commit(&a_empty[as]);
+            if (kc == p.nk - 1) tc_commit(&t_full[t]);
+            if (++as == p.na) { as = 0; aph ^= 1; }
+          }
+          tc_commit(&w_empty[wsl]);
+          if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
+        }
+        accph ^= (1u << T) - 1u;
+      }
+    }
+  } else if (warp <= 5) {
+    // ----------------------------------------------------------- RMS + epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = 32 * q + lane;
+    int as = 0, aph = 0, gi = 0;
+    uint32_t accph = 0;
+    for (int64_t g = blockIdx.x; g < NG; g += G) {
+      int64_t r0, r1;
+      group_range(g, n, n32, NG, r0, r1);
+      const int T = (int)((r1 - r0 + 127) / 128);
+      float ss0[4] = {0.f, 0.f, 0.f, 0.f}, ss1[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int kc = 0; kc < p.nk; ++kc) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (t < T) {
+            mbar_wait(&a_full[as], aph);
+            const uint8_t* rp = sA + (size_t)as * kASlotBytes + row * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint4 u = *reinterpret_cast<const uint4*>(rp + ((j ^ (row & 7)) << 4));
+              float f[8];
+              if (p.idesc & (1u << 7)) unpack16(u, f, (const __nv_bfloat16*)nullptr);
+              else unpack16(u, f, (const __half*)nullptr);
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                ss0[t] = fmaf(f[e], f[e], ss0[t]);
+                ss1[t] = fmaf(f[e + 1], f[e + 1], ss1[t]);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_empty[as]);
+            if (++as == p.na) { as = 0; aph ^= 1; }
+          }
+        }
+      }
+      const int par = gi & 1;
+      mbar_wait(&m_empty[par], (((uint32_t)gi >> 1) & 1u) ^ 1u);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        uint32_t bal = 0;
+        if (t < T) {
+          mbar_wait(&t_full[t], (accph >> t) & 1u);
+          tc_fence_after();
+          const int64_t r = r0 + (int64_t)t * 128 + row;
+          const bool valid = r < r1;
+          const float scale = rms_scale(ss0[t] + ss1[t], p.inv_d, p.eps);
+          float acc = 0.f;
+          const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(t * p.bp);
+          for (int c0 = 0; c0 < p.b; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(taddr + (uint32_t)c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              const int j = c0 + jj;
+              if (j < p.b) {
+                const float a = __fmul_rn(__uint_as_float(v[jj]), scale);
+                acc = fmaf(sWup[j], silu_f32(a), acc);
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_empty[t]);
+          const float score = score_from_logit(acc);
+          const bool ex = valid && (score > p.theta);
+          if (valid) {
+            if (p.scores) p.scores[r] = score;
+            if (p.logits) p.logits[r] = acc;
+            if (p.mask) p.mask[r] = ex ? 1 : 0;
+            if (ex && p.exit_layers) p.exit_layers[gathered ? p.row_idx[r] : r] = p.layer;
+          }
+          bal = __ballot_sync(0xffffffffu, ex);
+        }
+        if (lane == 0) words[par * 16 + t * 4 + q] = bal;
+      }
+      accph ^= (1u << T) - 1u;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m_full[par]);
+      ++gi;
+    }
+  } else {
+    // ----------------------------------------------------------- compaction
+    int gi = 0;
+    for (int64_t g = blockIdx.x; g < NG; g += G) {
+      int64_t r0, r1;
+      group_range(g, n, n32, NG, r0, r1);
+      const int par = gi & 1;
+      mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
+      const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m_empty[par]);
+      const uint32_t cnt = __popc(word);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl_w = incl - cnt;
+      const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+      if (need_scan) {
+        const uint32_t E = lookback_exclusive(p.ws->status, tag, g, agg);
+        if (p.exit_idx || p.cont_idx) {
+          const int nwords = (int)((r1 - r0 + 31) / 32);
+          const uint32_t lt = (1u << lane) - 1u;
+          for (int w = 0; w < nwords; ++w) {
+            const uint32_t wd = __shfl_sync(0xffffffffu, word, w);
+            const uint32_t pre = __shfl_sync(0xffffffffu, excl_w, w);
+            const int64_t r = r0 + 32 * w + lane;
+            if (r < r1) {
+              const int64_t rank = (int64_t)E + pre + __popc(wd & lt);
+              const int64_t id = (p.ids_from_rows && gathered) ? p.row_idx[r] : r;
+              if ((wd >> lane) & 1u) {
+                if (p.exit_idx) p.exit_idx[rank] = id;
+              } else if (p.cont_idx) {
+                p.cont_idx[r - rank] = id;
+              }
+            }
+          }
+        }
+        if (g == NG - 1 && lane == 0 && p.counts) {
+          p.counts[0] = (int64_t)E + agg;
+          p.counts[1] = n - ((int64_t)E + agg);
+        }
+      }
+      ++gi;
+    }
+    if (NG == 0 && blockIdx.x == 0 && lane == 0 && p.counts) {
+      p.counts[0] = 0;
+      p.counts[1] = 0;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+  if (threadIdx.x == 0) launch_done(p.ws);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+static int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, int64_t rows,
+                    int64_t ld_elems, int box_cols, int box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return set_error(TIDE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ld_elems * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = enc(m, dtype == TIDE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   2, const_cast<void*>(base), gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(TIDE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TIDE_OK;
+}
+
+bool route_tc_supported(int dtype, int d, int b) {
+  return (dtype == TIDE_BF16 || dtype == TIDE_F16) && d >= 8 && d % 8 == 0 && b >= 1 &&
+         b <= 256;
+}
+
+int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
+  const int npad = (a.b + 15) / 16 * 16;
+  const int bp = (npad + 31) / 32 * 32;
+  const int tpg = std::min(4, 512 / bp);
+  int cols = 32;
+  while (cols < tpg * bp) cols <<= 1;
+  const int nk = (a.d + 63) / 64;
+  const uint32_t wslot = (uint32_t)npad * 128u;
+  const int nw = npad <= 128 ? 4 : 3;
+  // smem carve-up (offsets from a 1024-aligned base)
+  const uint32_t off_a = (uint32_t)nw * wslot;
+  const int smem_cap = 227 * 1024;
+  const uint32_t misc = 1024 /*w_up*/ + 512 /*bars*/ + 128 /*words*/ + 2048 /*ids*/ + 16;
+  int na = (int)((smem_cap - 1024 - off_a - misc) / kASlotBytes);
+  na = std::min(na, kMaxNA);
+  if (na < 2) return set_error(TIDE_ERR_UNSUPPORTED, "bottleneck too wide for smem");
+  TcParams p{};
+  p.n_host = a.n;
+  p.n_dev = a.n_dev;
+  p.rows_total = a.rows_total;
+  p.d = a.d;
+  p.b = a.b;
+  p.npad = npad;
+  p.bp = bp;
+  p.tpg = tpg;
+  p.nk = nk;
+  p.na = na;
+  p.nw = nw;
+  p.idesc = f16_idesc(a.dtype == TIDE_BF16 ? 1 : 0, 128, npad);
+  p.tmem_cols = (uint32_t)cols;
+  p.wslot = wslot;
+  p.off_a = off_a;
+  p.off_wup = off_a + (uint32_t)na * kASlotBytes;
+  p.off_bar = p.off_wup + 1024;
+  p.off_words = p.off_bar + 512;
+  p.off_ids = p.off_words + 128;
+  p.off_tmem = p.off_ids + 2048;
+  const uint32_t smem_bytes = p.off_tmem + 16 + 1024;
+  p.row_idx = a.row_idx;
+  p.ids_from_rows = a.ids_from_rows;
+  p.w_up = a.w_up;
+  p.eps = a.eps;
+  p.inv_d = (float)(1.0 / (double)a.d);
+  p.theta = a.theta;
+  p.layer = a.layer;
+  p.scores = a.scores;
+  p.logits = a.logits;
+  p.mask = a.mask;
+  p.exit_idx = a.exit_idx;
+  p.cont_idx = a.cont_idx;
+  p.exit_layers = a.exit_layers;
+  p.counts = a.counts;
+  p.ws = reinterpret_cast<Workspace*>(a.workspace);
+
+  CUtensorMap tm_h128, tm_h32, tm_w, tm_g4;
+  const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
+  int rc;
+  if ((rc = make_map(&tm_h128, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
+  if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 32))) return rc;
+  if ((rc = make_map(&tm_g4, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 1))) return rc;
+  if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
+
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = sm_count(dev);
+  const int64_t n32 = (a.n + 31) / 32;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n32));
+  static bool attr_set[64] = {false};
+  if (!attr_set[dev & 63]) {
+    cudaFuncSetAttribute(route_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr_set[dev & 63] = true;
+  }
+  route_tc_kernel<<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h32, tm_w, tm_g4, p);
+  return check_launch("route_tc_kernel");
+}
+
+}  // namespace tide

@@ -1,0 +1,264 @@
+"""Post-hoc exit selection on B200 (ee/runtime.py:28-181).
+
+`posthoc_select` keeps the reference signature and results:
+(logits [n, vocab] f32, exit_layers [n] int64, NO_EXIT = -1).  On the device:
+
+  * per-token, n > 16: one fused route+compact launch per checkpoint >= k_min;
+    checkpoint k+1 gathers only the rows still remaining (TMA tile::gather4 on
+    the previous launch's continuing indices) and reads the remaining count
+    from device memory, so the chain never syncs the host;
+  * n <= 16 (decode): every checkpoint in ONE launch + in-kernel resolution
+    (a row's score at checkpoint k depends only on that row, so the first
+    firing checkpoint is exactly what peeling computes);
+  * batch-unanimous, n > 16: one launch per checkpoint until all rows fire;
+  * then one select_project launch final-norms every row from its exit layer
+    (exit_projection + the final-rows rmsnorm of ee/runtime.py:176,180) and
+    cuBLAS multiplies by the LM head.
+
+`model` is anything with .config.num_layers, .config.hidden_dim, .final_norm
+and .lm_head — the reference's ReferenceModel, or `OutputHead` below.  `bank`
+is this package's RouterBank or the reference's.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _native as N
+from .router_ops import _NoTF32, device_weights
+from .tensor_math import DEFAULT_EPS
+
+PER_TOKEN = "per-token"
+BATCH_UNANIMOUS = "batch-unanimous"
+MODES = (PER_TOKEN, BATCH_UNANIMOUS)
+FINAL_KEY = "final"
+NO_EXIT = -1
+
+
+@dataclass(frozen=True)
+class RuntimeConfig:
+    """ee/runtime.py:38-56 (same validation)."""
+
+    exit_threshold: float = 1.0
+    k_min: int = 0
+    mode: str = PER_TOKEN
+    max_new_tokens: int = 64
+    temperature: float = 0.0
+
+    def __post_init__(self):
+        if not 0.0 < self.exit_threshold <= 1.0:
+            raise ValueError("exit_threshold must lie in (0, 1]")
+        if self.k_min < 0:
+            raise ValueError("k_min must be >= 0")
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}")
+        if self.max_new_tokens < 1:
+            raise ValueError("max_new_tokens must be >= 1")
+        if self.temperature < 0.0:
+            raise ValueError("temperature must be >= 0")
+
+
+@dataclass
+class PhaseStats:
+    """Exit accounting for one phase (ee/runtime.py:59-92)."""
+
+    tokens_total: int
+    exit_layers: list
+    histogram: dict
+    exit_rate: float
+
+    @classmethod
+    def from_exit_layers(cls, exit_layers: Sequence[int]) -> "PhaseStats":
+        if isinstance(exit_layers, torch.Tensor):
+            exit_layers = exit_layers.detach().cpu().tolist()
+        layers = [int(k) for k in exit_layers]
+        histogram: dict = {}
+        for k in layers:
+            key = FINAL_KEY if k == NO_EXIT else k
+            histogram[key] = histogram.get(key, 0) + 1
+        exited = sum(1 for k in layers if k != NO_EXIT)
+        total = len(layers)
+        return cls(tokens_total=total, exit_layers=layers, histogram=histogram,
+                   exit_rate=(exited / total) if total else 0.0)
+
+    def to_dict(self) -> dict:
+        histogram = {str(key): self.histogram[key]
+                     for key in sorted(self.histogram,
+                                       key=lambda k: (1, 0) if k == FINAL_KEY else (0, k))}
+        return {"tokens_total": self.tokens_total, "exit_rate": self.exit_rate,
+                "histogram": histogram,
+                "exit_layers": [None if k == NO_EXIT else k for k in self.exit_layers]}
+
+
+@dataclass
+class OutputHead:
+    """The part of a model posthoc_select touches: depth, width, final norm gain, LM head."""
+
+    num_layers: int
+    hidden_dim: int
+    final_norm: object  # [d]
+    lm_head: object  # [vocab, d]
+
+    @property
+    def config(self):
+        return self
+
+
+_head_cache: dict = {}
+
+
+def _device_head(model, dev):
+    key = (id(model), dev.index)
+    fn, lm = model.final_norm, model.lm_head
+    hit = _head_cache.get(key)
+    if hit is not None and hit[0] is fn and hit[1] is lm:
+        return hit[2], hit[3]
+    g = D.to_device_f32(fn, dev).reshape(-1)
+    w = D.to_device_f32(lm, dev)
+    _head_cache[key] = (fn, lm, g, w, model)
+    return g, w
+
+
+def _check_bank(model, hidden_states, bank) -> None:
+    """ee/runtime.py:120-131 (same messages)."""
+    if len(hidden_states) != bank.num_layers + 1:
+        raise ValueError(
+            f"got {len(hidden_states)} hidden states, bank expects "
+            f"{bank.num_layers + 1} (embedding + one per layer)")
+    if hidden_states[0].shape[-1] != bank.hidden_dim:
+        raise ValueError(
+            f"hidden width {hidden_states[0].shape[-1]} != bank width {bank.hidden_dim}")
+    if model.config.num_layers != bank.num_layers:
+        raise ValueError(
+            f"model has {model.config.num_layers} layers, bank was calibrated for "
+            f"{bank.num_layers}")
+
+
+def _stage_layers(hidden_states, needed: Sequence[int]):
+    """Device tensors for the capture indices in `needed`, one common dtype."""
+    dev = None
+    for h in hidden_states:
+        if isinstance(h, torch.Tensor) and h.is_cuda:
+            dev = h.device
+            break
+    dev = dev or torch.device("cuda", torch.cuda.current_device())
+    out = {}
+    for i in needed:
+        h = hidden_states[i]
+        t = D.to_device_f32(h, dev) if D.is_host(h) else h
+        if t.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+            t = t.float()
+        out[i] = t
+    if len({t.dtype for t in out.values()}) > 1:
+        out = {i: t.float() for i, t in out.items()}
+    for i, t in out.items():
+        if t.dim() != 2:
+            raise ValueError(f"hidden state {i} must be [n, d], got {tuple(t.shape)}")
+        out[i] = t.contiguous()
+    return out, dev
+
+
+def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
+                 staged=None, dev=None):
+    """Exit map only (int64 CUDA tensor [n]); the hot path of posthoc_select."""
+    L = bank.num_layers
+    ckpts = [k for k in bank.checkpoints if k >= config.k_min]
+    if staged is None:
+        staged, dev = _stage_layers(hidden_states, [k + 1 for k in ckpts] + [L])
+    final = staged[L]
+    n, d = final.shape
+    exit_layers = torch.full((n,), NO_EXIT, dtype=torch.int64, device=dev)
+    if not ckpts or n == 0:
+        return exit_layers
+    lib = N.load()
+    s = D.stream_handle(dev)
+    ws = D.workspace(dev).data_ptr()
+    theta = float(np.float32(config.exit_threshold))
+    eps = float(np.float32(bank.eps))
+    code = D.dtype_code(final)
+    b = bank.bottleneck if hasattr(bank, "bottleneck") else bank.routers[ckpts[0]].bottleneck
+    if n <= N.MAX_DECODE_ROWS:
+        ws_w = [device_weights(bank.routers[k], code, dev) for k in ckpts]
+        mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
+        cnt = torch.empty(1, dtype=torch.int64, device=dev)
+        N.check(lib.tide_route_decode(
+            N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
+            N.ptr_array([w.data_ptr() for w, _ in ws_w]),
+            N.ptr_array([u.data_ptr() for _, u in ws_w]), b, N.i64_array(ckpts), eps, theta,
+            int(config.k_min), mode, None, None, exit_layers.data_ptr(), cnt.data_ptr(), ws, s),
+            "tide_route_decode")
+        return exit_layers
+    if config.mode == BATCH_UNANIMOUS:
+        counts = torch.empty(2, dtype=torch.int64, device=dev)
+        for k in ckpts:
+            wd, wu = device_weights(bank.routers[k], code, dev)
+            N.check(lib.tide_route(staged[k + 1].data_ptr(), d, n, None, n, d, code, None,
+                                   wd.data_ptr(), wu.data_ptr(), b, eps, theta, k, None, None,
+                                   None, None, None, 0, None, counts.data_ptr(), ws, s),
+                    "tide_route")
+            if int(counts[0].item()) == n:
+                exit_layers.fill_(k)
+                break
+        return exit_layers
+    rem = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
+    cnt = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(2)]
+    row_idx, n_dev = 0, 0
+    for i, k in enumerate(ckpts):
+        wd, wu = device_weights(bank.routers[k], code, dev)
+        h = staged[k + 1]
+        N.check(lib.tide_route(h.data_ptr(), d, n, n_dev or None, n, d, code, row_idx or None,
+                               wd.data_ptr(), wu.data_ptr(), b, eps, theta, k, None, None, None,
+                               None, rem[i & 1].data_ptr(), 1, exit_layers.data_ptr(),
+                               cnt[i & 1].data_ptr(), ws, s), "tide_route")
+        row_idx = rem[i & 1].data_ptr()
+        n_dev = cnt[i & 1].data_ptr() + 8
+    return exit_layers
+
+
+def posthoc_select(model, hidden_states, bank, config: RuntimeConfig, *,
+                   return_logits: bool = True):
+    """Select output logits per the post-hoc exit rule (ee/runtime.py:134-181).
+
+    hidden_states[0] is the embedding output, hidden_states[k+1] the output of
+    layer k.  Returns (logits [n, vocab], exit_layers [n]); NO_EXIT marks rows
+    that used the final layer.  With bank=None this is the baseline output."""
+    host = all(D.is_host(h) for h in hidden_states)
+    D.require_cuda()
+    L = model.config.num_layers
+    if bank is not None:
+        _check_bank(model, hidden_states, bank)
+        ckpts = [k for k in bank.checkpoints if k >= config.k_min]
+    else:
+        ckpts = []
+    needed = sorted(set([k + 1 for k in ckpts] + [len(hidden_states) - 1]))
+    staged, dev = _stage_layers(hidden_states, needed)
+    final = staged[len(hidden_states) - 1]
+    n, d = final.shape
+    if d != model.config.hidden_dim:
+        raise ValueError(f"hidden width {d} != model width {model.config.hidden_dim}")
+    if bank is None:
+        exit_layers = torch.full((n,), NO_EXIT, dtype=torch.int64, device=dev)
+    else:
+        exit_layers = select_exits(hidden_states, bank, config, staged=staged, dev=dev)
+    logits = None
+    if return_logits:
+        gain, lm = _device_head(model, dev)
+        normed = torch.empty((n, d), dtype=torch.float32, device=dev)
+        ptrs = [0] * len(hidden_states)
+        for i, t in staged.items():
+            ptrs[i] = t.data_ptr()
+        if n:
+            N.check(N.load().tide_select_project(
+                N.ptr_array(ptrs), len(ptrs), d, D.dtype_code(final), exit_layers.data_ptr(), n,
+                d, gain.data_ptr(), float(np.float32(DEFAULT_EPS)), normed.data_ptr(), d,
+                D.stream_handle(dev)), "tide_select_project")
+        with _NoTF32():
+            logits = normed @ lm.t()
+    if host:
+        return (D.to_host(logits) if logits is not None else None), D.to_host(exit_layers)
+    return logits, exit_layers

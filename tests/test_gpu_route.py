@@ -1,0 +1,198 @@
+"""GPU parity: fused RMSNorm + router + mask + compaction vs the oracle and the
+reference's golden vectors (restates pkg/tests/test_router_ops.py:72-107 and
+test_acceptance.py #2 against the kernels)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_21365_b200 as P
+from paper_2603_21365_b200 import _device as D
+from paper_2603_21365_b200 import _native as N
+from oracle import tide_oracle as O
+from tests.golden.cases import ROUTE_CASES, digest, make_route_inputs, stored_digest
+from tests.gpu_helpers import (check_decisions, check_logits, need_gpu, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+def _router(wd, wu, layer=3):
+    return P.Router(layer=layer, w_down=wd, w_up=wu)
+
+
+@pytest.mark.parametrize("name", sorted(ROUTE_CASES))
+def test_route_case_matches_oracle_and_golden(golden_route, name):
+    need_gpu()
+    spec = ROUTE_CASES[name]
+    h, wd, wu = make_route_inputs(spec)
+    assert digest(h, wd, wu) == stored_digest(golden_route, f"{name}__digest")
+    router = _router(wd, wu)
+    oref = O.OracleRouter(3, wd, wu)
+    s_ref, t_ref, m_ref = O.route_logits(h, oref)
+    dt = spec["dtype"]
+    x = to_dev(h, dt)
+    r = P.route(x, router, theta=0.5, want_logits=True, want_indices=True)
+    scores = r["scores"].cpu().numpy()
+    logits = r["logits"].cpu().numpy()
+    check_logits(logits, t_ref, m_ref, dt, name)
+    # scores are sigma(logit) in f64 -> f32, bounded in [0, 1]
+    assert np.all(scores >= 0) and np.all(scores <= 1)
+    np.testing.assert_array_equal(scores, np.array([O._sigma64(float(v)) for v in logits],
+                                                   np.float32))
+    if dt == "f32":
+        # reference criterion #2 (test_acceptance.py:70-87): within 1e-5 of the reference
+        assert np.max(np.abs(scores - golden_route[f"{name}__fused"])) <= 1e-5
+    mask = r["mask"].cpu().numpy()
+    check_decisions(mask, t_ref, m_ref, 0.5, dt, name)
+    # compaction is bit-exact against the oracle applied to the GPU's own mask
+    e, c = O.compact_indices(mask)
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+    if spec["kind"] == "rigged":
+        zero = set(spec.get("zero_rows", ()))
+        for i in range(spec["n"]):
+            want = 0.5 if i in zero else (1.0 if spec["hot"] else 0.0)
+            assert scores[i] == want, (i, scores[i], want)
+
+
+@pytest.mark.parametrize("theta", [1.0, 0.85, 0.5, 0.1])
+def test_threshold_rule_and_off_switch(theta):
+    need_gpu()
+    h, wd, wu = make_route_inputs(ROUTE_CASES["bf16_4096x128"])
+    router = _router(wd, wu)
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, "bf16"), router, theta=theta, want_indices=True)
+    mask = r["mask"].cpu().numpy()
+    check_decisions(mask, t_ref, m_ref, theta, "bf16", f"theta={theta}")
+    if theta == 1.0:
+        assert not mask.any()
+        assert r["exiting_indices"].numel() == 0
+
+
+def test_host_api_matches_reference_semantics(rng):
+    """pkg/tests/test_router_ops.py:72-107 restated on the kernels (host numpy API)."""
+    need_gpu()
+    router = P.Router(layer=3, w_down=rng.standard_normal((32, 64), dtype=np.float32),
+                      w_up=rng.standard_normal((1, 32), dtype=np.float32))
+    h = rng.standard_normal((200, 64), dtype=np.float32) * 5
+    fused = P.fused_layernorm_route(h, router)
+    assert isinstance(fused, np.ndarray) and fused.dtype == np.float32
+    composed = P.route_scores(h, router)
+    assert np.max(np.abs(fused - composed)) <= 1e-5
+    big = P.fused_layernorm_route(h * 100, router)
+    assert np.all(big >= 0.0) and np.all(big <= 1.0)
+    assert P.fused_layernorm_route(np.zeros((1, 64), np.float32), router)[0] == 0.5
+    a = P.fused_layernorm_route(h[:10], router)
+    b = P.fused_layernorm_route(h[:10] * 1000.0, router)
+    np.testing.assert_allclose(a, b, atol=1e-5)
+    with pytest.raises(ValueError, match="expected"):
+        P.fused_layernorm_route(np.zeros((3, 32), np.float32), router)
+    assert P.fused_layernorm_route(np.zeros((0, 64), np.float32), router).shape == (0,)
+
+
+def test_tensor_core_path_selected():
+    need_gpu()
+    lib = N.load()
+    assert lib.tide_route_uses_tensor_cores(N.BF16, 4096, 128) == 1
+    assert lib.tide_route_uses_tensor_cores(N.F16, 8192, 256) == 1
+    assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 128) == 0
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 127, 128, 129, 500, 4099, 20000])
+def test_ragged_sizes_bf16(n):
+    """Every tile / group boundary: 32-row boxes, partial tiles, multi-group CTAs."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(1000 + n))
+    d, b = 512, 128
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.05).astype(np.float32)
+    h = O.round_to(g.standard_normal((n, d), dtype=np.float32), "bf16")
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, "bf16"), _router(wd, wu), theta=0.5, want_logits=True,
+                want_indices=True)
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, "bf16", f"n={n}")
+    mask = r["mask"].cpu().numpy()
+    e, c = O.compact_indices(mask)
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+def test_gathered_rows_equal_dense_on_subset():
+    """row_idx (peeling) mode == dense route over h[row_idx]; ids mapped back."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(77))
+    n, d, b = 3000, 1024, 128
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.05).astype(np.float32)
+    h = O.round_to(g.standard_normal((n, d), dtype=np.float32), "bf16")
+    x = to_dev(h, "bf16")
+    router = _router(wd, wu)
+    sub = np.sort(g.choice(n, size=1777, replace=False)).astype(np.int64)
+    wdd, wud = P.router_ops.device_weights(router, N.BF16, x.device)
+    m = len(sub)
+    idx = torch.from_numpy(sub).cuda()
+    logits = torch.empty(m, dtype=torch.float32, device="cuda")
+    mask = torch.empty(m, dtype=torch.uint8, device="cuda")
+    cont = torch.empty(m, dtype=torch.int64, device="cuda")
+    ex = torch.empty(m, dtype=torch.int64, device="cuda")
+    counts = torch.empty(2, dtype=torch.int64, device="cuda")
+    exit_layers = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    lib = N.load()
+    N.check(lib.tide_route(x.data_ptr(), d, m, None, n, d, N.BF16, idx.data_ptr(),
+                           wdd.data_ptr(), wud.data_ptr(), b, 1e-6, 0.5, 9, None,
+                           logits.data_ptr(), mask.data_ptr(), ex.data_ptr(), cont.data_ptr(), 1,
+                           exit_layers.data_ptr(), counts.data_ptr(),
+                           D.workspace().data_ptr(), D.stream_handle()), "tide_route")
+    dense = P.route(x[idx], router, theta=0.5, want_logits=True)
+    np.testing.assert_array_equal(logits.cpu().numpy(), dense["logits"].cpu().numpy())
+    mk = mask.cpu().numpy().astype(bool)
+    ne = int(counts[0])
+    assert ne == mk.sum() and int(counts[1]) == m - ne
+    np.testing.assert_array_equal(ex.cpu().numpy()[:ne], sub[mk])
+    np.testing.assert_array_equal(cont.cpu().numpy()[: m - ne], sub[~mk])
+    el = exit_layers.cpu().numpy()
+    assert np.all(el[sub[mk]] == 9) and np.all(el[np.setdiff1d(np.arange(n), sub[mk])] == -1)
+
+
+def test_device_count_input():
+    """n read from device memory (the peeling chain's counts[1])."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(78))
+    n, d, b = 1000, 256, 64
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.05).astype(np.float32)
+    h = O.round_to(g.standard_normal((n, d), dtype=np.float32), "bf16")
+    x = to_dev(h, "bf16")
+    router = _router(wd, wu)
+    wdd, wud = P.router_ops.device_weights(router, N.BF16, x.device)
+    for live in (0, 1, 37, 640, 1000):
+        ndev = torch.tensor([0, live], dtype=torch.int64, device="cuda")
+        logits = torch.full((n,), 7.0, dtype=torch.float32, device="cuda")
+        counts = torch.full((2,), -5, dtype=torch.int64, device="cuda")
+        N.check(N.load().tide_route(x.data_ptr(), d, n, ndev.data_ptr() + 8, n, d, N.BF16, None,
+                                    wdd.data_ptr(), wud.data_ptr(), b, 1e-6, 0.5, 1, None,
+                                    logits.data_ptr(), None, None, None, 0, None,
+                                    counts.data_ptr(), D.workspace().data_ptr(),
+                                    D.stream_handle()), "tide_route")
+        lg = logits.cpu().numpy()
+        assert np.all(lg[live:] == 7.0)
+        if live:
+            ref = P.route(x[:live], router, want_logits=True)["logits"].cpu().numpy()
+            np.testing.assert_array_equal(lg[:live], ref)
+        assert int(counts[0]) + int(counts[1]) == live
+
+
+def test_repeated_launches_reuse_workspace():
+    """The epoch-tagged look-back state needs no reset between launches."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(79))
+    n, d, b = 9000, 256, 128
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.05).astype(np.float32)
+    router = _router(wd, wu)
+    for it in range(6):
+        h = O.round_to(g.standard_normal((n, d), dtype=np.float32), "bf16")
+        r = P.route(to_dev(h, "bf16"), router, theta=0.5, want_indices=True)
+        e, c = O.compact_indices(r["mask"].cpu().numpy())
+        np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+        np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)

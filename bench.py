@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the TIDE exit-decision hot path on B200 (driver contract).
+
+Headline (BASELINE.json metric): routed tokens/s of the fused
+RMSNorm + router + exit mask + stable compaction at d=4096 bf16, b=128, one
+checkpoint, 65,536 tokens per GPU (weak scaling), theta=0.5, dense rows, and
+its fraction of the HBM roofline.  One step = one tide_route launch over the
+resident batch (+ for N>1 the exit-map / compacted-index all-gathers over
+NCCL).  Inputs are 512 MiB per step, larger than the 126 MB L2, so no flush.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--extra]
+
+`--impl reference` times the reference algorithm on the host cores instead
+(the oracle port of ee/router_ops.py:68-87 + ee/runtime.py:171 +
+ee/router_ops.py:137-154, token-sharded over worker processes).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "routed tokens/sec at d=4096 bf16 (fused norm+router+compact); % HBM roofline"
+UNIT = "tokens/s"
+N_TOK, D, B, THETA, EPS = 65536, 4096, 128, 0.5, 1e-6
+ELEM = 2
+# algorithmic bytes per routed token: row + f32 score + u8 mask + int64 index
+BYTES_PER_TOKEN = D * ELEM + 4 + 1 + 8
+WEIGHT_BYTES = B * D * ELEM + B * 4
+
+
+def workload_config(n_gpus: int) -> dict:
+    return {"workload": "fused RMSNorm+router+exit-mask+stable-compaction, 1 checkpoint, "
+                        "65,536 tokens/GPU, d=4096, b=128, bf16 rows+W_down, f32 w_up, "
+                        "theta=0.5, dense (no row index)",
+            "tokens_per_gpu": N_TOK, "d": D, "b": B, "theta": THETA,
+            "global_tokens": N_TOK * n_gpus, "parallelism": f"token-sharded x{n_gpus}",
+            "l2": "inputs 512 MiB per step per GPU > 126 MB L2 (no flush needed)",
+            "router_init": "N(0,1)*0.05, PCG64(202)", "rows": "N(0,1) bf16, torch cuda "
+                                                             "Generator seeded 1234+rank"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        time.sleep(0.25)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=1)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        load = [x for x in sm if x > 300] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(kernel)
+    return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference / baseline (oracle port, token-sharded over processes)
+# ---------------------------------------------------------------------------
+def _cpu_worker(args):
+    seed, rows, d, b = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import tide_oracle as O
+    g = np.random.Generator(np.random.PCG64(202))
+    router = O.make_router(d, b, 3, g)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    h = O.round_to(rng.standard_normal((rows, d), dtype=np.float32), "bf16")
+    t0 = time.perf_counter()
+    scores = O.fused_layernorm_route(h, router)           # ee/router_ops.py:68-87
+    mask = scores > np.float32(THETA)                     # ee/runtime.py:171
+    O.batch_compact(h, mask)                              # ee/router_ops.py:137-154
+    return rows, time.perf_counter() - t0
+
+
+class CpuReference:
+    """The reference algorithm timed on this host's cores: one worker process
+    per core (OPENBLAS_NUM_THREADS=1 each), token-sharded bounded samples."""
+
+    def __init__(self, cores=None):
+        import multiprocessing as mp
+        self.cores = cores or os.cpu_count() or 1
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        self.pool = mp.get_context("spawn").Pool(self.cores)
+        rows, dt = self.pool.map(_cpu_worker, [(7, 128, D, B)] * self.cores)[0]
+        self.per_proc = rows / max(dt, 1e-9)
+
+    def sample(self, target_s: float) -> dict:
+        rows_each = int(max(64, min(65536, self.per_proc * target_s)))
+        rows_each = int(math.ceil(rows_each / 64) * 64)
+        res = self.pool.map(_cpu_worker, [(100 + i, rows_each, D, B) for i in range(self.cores)])
+        total = sum(r for r, _ in res)
+        slowest = max(t for _, t in res)
+        return {"value": total / slowest, "unit": UNIT, "cores": self.cores, "kind": "port",
+                "sample": f"{self.cores} processes x {rows_each} tokens (d=4096, bf16-rounded "
+                          f"rows as f32; per-row reference loop + strict mask + batch_compact)",
+                "tokens": total, "seconds": slowest}
+
+    def close(self):
+        self.pool.terminate()
+
+
+def cpu_reference_rate(target_s: float = 10.0) -> dict:
+    ref = CpuReference()
+    try:
+        return ref.sample(target_s)
+    finally:
+        ref.close()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    ref = CpuReference()
+    step_s = float(os.environ.get("TIDE_REF_STEP_S", max(0.5, 100.0 / (args.steps + args.warmup))))
+    try:
+        runs = [ref.sample(step_s) for _ in range(args.warmup + args.steps)][args.warmup:]
+    finally:
+        ref.close()
+    rate = sum(x["tokens"] for x in runs) / sum(x["seconds"] for x in runs)
+    line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(x["seconds"] for x in runs) / len(runs),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload_config(1), "impl": "reference",
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": runs[-1]["cores"],
+                             "kind": "port", "sample": runs[-1]["sample"]},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2603_21365_b200 as P
+    from paper_2603_21365_b200 import _device as Dv
+    from paper_2603_21365_b200 import _native as N
+    from paper_2603_21365_b200 import sharding as S
+    from oracle import tide_oracle as O
+
+    g = np.random.Generator(np.random.PCG64(202))
+    orouter = O.make_router(D, B, 3, g)
+    router = P.Router(layer=3, w_down=orouter.w_down, w_up=orouter.w_up)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    h = torch.randn((N_TOK, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    wd, wu = P.router_ops.device_weights(router, N.BF16, dev)
+    scores = torch.empty(N_TOK, dtype=torch.float32, device=dev)
+    mask = torch.empty(N_TOK, dtype=torch.uint8, device=dev)
+    exit_idx = torch.empty(N_TOK, dtype=torch.int64, device=dev)
+    cont_idx = torch.empty(N_TOK, dtype=torch.int64, device=dev)
+    counts = torch.empty(2, dtype=torch.int64, device=dev)
+    lib = N.load()
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    ws = Dv.workspace(dev).data_ptr()
+    gathered = S.ExitMapGather(N_TOK, world, dev) if world > 1 else None
+    launches = {"n": 0}
+
+    def step(kernel_events=None):
+        if kernel_events is not None:
+            kernel_events[0].record(stream)
+        rc = lib.tide_route(h.data_ptr(), D, N_TOK, None, N_TOK, D, N.BF16, None, wd.data_ptr(),
+                            wu.data_ptr(), B, EPS, THETA, 3, scores.data_ptr(), None,
+                            mask.data_ptr(), exit_idx.data_ptr(), cont_idx.data_ptr(), 0, None,
+                            counts.data_ptr(), ws, sh)
+        launches["n"] += 1
+        if kernel_events is not None:
+            kernel_events[1].record(stream)
+        if rc:
+            N.check(rc, "tide_route")
+        if gathered is not None:
+            gathered.all_gather(mask, exit_idx, counts, rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    # parity spot-check of the warm state on rank 0 (first 2,048 rows vs the oracle)
+    if rank == 0 and not args.no_check:
+        hs = h[:2048].float().cpu().numpy()
+        _, t_ref, m_ref = O.route_logits(hs, orouter)
+        ok = O.decision_band_ok(mask[:2048].cpu().numpy(), t_ref, m_ref, THETA, 2e-2)
+        assert ok.all(), "bench parity spot-check failed"
+        e_ref, _ = O.compact_indices(mask.cpu().numpy())
+        assert np.array_equal(exit_idx[: int(counts[0])].cpu().numpy(), e_ref)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches["n"] = 0
+    t0.record(stream)
+    for i in range(args.steps):
+        step(kev[i])
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    gpu_launches = launches["n"]
+    clk = clocks.stop()
+    ms_total = t0.elapsed_time(t1)
+    kernel_ms = [a.elapsed_time(b) for a, b in kev]
+    ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    ms_per_step = ms_max / args.steps
+    value = N_TOK * world * args.steps / (ms_max / 1e3)
+
+    # e2e through the public API with HOST buffers (pinned), copies in the timed region
+    h_host = h.cpu().pin_memory()
+    mask_host = torch.empty(N_TOK, dtype=torch.uint8).pin_memory()
+    idx_host = torch.empty(N_TOK, dtype=torch.int64).pin_memory()
+    cnt_host = torch.empty(2, dtype=torch.int64).pin_memory()
+    h_dev = torch.empty_like(h)
+
+    def e2e_fused_step():
+        h_dev.copy_(h_host, non_blocking=True)
+        rc = lib.tide_route(h_dev.data_ptr(), D, N_TOK, None, N_TOK, D, N.BF16, None,
+                            wd.data_ptr(), wu.data_ptr(), B, EPS, THETA, 3, scores.data_ptr(),
+                            None, mask.data_ptr(), exit_idx.data_ptr(), cont_idx.data_ptr(), 0,
+                            None, counts.data_ptr(), ws, sh)
+        N.check(rc, "tide_route")
+        mask_host.copy_(mask, non_blocking=True)
+        idx_host.copy_(exit_idx, non_blocking=True)
+        cnt_host.copy_(counts, non_blocking=True)
+
+    for _ in range(2):
+        e2e_fused_step()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(2, min(args.steps, 10))
+    barrier()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_fused_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = N_TOK * world * e2e_steps / (float(e_ms.item()) / 1e3)
+
+    if rank == 0:
+        peaks = measured_peaks()
+        kavg = sum(kernel_ms) / len(kernel_ms)
+        alg_bytes = N_TOK * BYTES_PER_TOKEN + WEIGHT_BYTES
+        achieved = alg_bytes / (kavg / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic", "config": workload_config(world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                         "traffic": ncu_traffic("route_tc_kernel"),
+                         "peak_src": peaks["src"], "kernel_ms": kavg,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "frac_of_8TBs_spec": achieved / 8000.0},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": N_TOK * D * ELEM,
+                    "d2h_bytes_per_step": N_TOK * 1 + N_TOK * 8 + 16},
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+            "extra": {"tensor_cores": bool(lib.tide_route_uses_tensor_cores(N.BF16, D, B)),
+                      "tflops_tensor": 2.0 * D * B * N_TOK / (kavg / 1e3) / 1e12,
+                      "kernel_ms_min": min(kernel_ms), "kernel_ms_max": max(kernel_ms)},
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(
+                float(os.environ.get("TIDE_CPU_BASELINE_S", "10"))).items()
+                if k in ("value", "unit", "cores", "kind", "sample")}
+        if args.extra:
+            from bench_extra import run_extra
+            line["extra"]["configs"] = run_extra(dev)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--extra", action="store_true", help="also time configs 2-5 (slower)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -70,6 +70,7 @@ __device__ __forceinline__ void group_range(int64_t g, int64_t n, int64_t n32, i
   if (r1 > n) r1 = n;
 }
 
+template <bool kBF16>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     route_tc_kernel(const __grid_constant__ CUtensorMap tm_h128,
                     const __grid_constant__ CUtensorMap tm_h32,
@@ -225,40 +226,58 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // ----------------------------------------------------------- RMS + epilogue
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = 32 * q + lane;
+    const uint32_t swz = (uint32_t)(row & 7);
     int as = 0, aph = 0, gi = 0;
     uint32_t accph = 0;
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
       group_range(g, n, n32, NG, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
-      float ss0[4] = {0.f, 0.f, 0.f, 0.f}, ss1[4] = {0.f, 0.f, 0.f, 0.f};
+      // sum of squares of this thread's row, per tile, from the swizzled A slots
+      f32x2 ss[4][2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ss[t][0] = ss[t][1] = 0ull;
       for (int kc = 0; kc < p.nk; ++kc) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           if (t < T) {
             mbar_wait(&a_full[as], aph);
             const uint8_t* rp = sA + (size_t)as * kASlotBytes + row * 128;
+            uint4 u[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint4 u = *reinterpret_cast<const uint4*>(rp + ((j ^ (row & 7)) << 4));
-              float f[8];
-              if (p.idesc & (1u << 7)) unpack16(u, f, (const __nv_bfloat16*)nullptr);
-              else unpack16(u, f, (const __half*)nullptr);
-#pragma unroll
-              for (int e = 0; e < 8; e += 2) {
-                ss0[t] = fmaf(f[e], f[e], ss0[t]);
-                ss1[t] = fmaf(f[e + 1], f[e + 1], ss1[t]);
-              }
-            }
+            for (int j = 0; j < 8; ++j)
+              u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_empty[as]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                f32x2 x;
+                if (kBF16) {
+                  x = pack2u(w[e] << 16, w[e] & 0xFFFF0000u);
+                } else {
+                  const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+                  x = pack2(f2.x, f2.y);
+                }
+                ss[t][e & 1] = ffma2(x, x, ss[t][e & 1]);
+              }
+            }
             if (++as == p.na) { as = 0; aph ^= 1; }
           }
         }
       }
+      float ssum[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float a0, a1, b0, b1;
+        unpack2(ss[t][0], a0, a1);
+        unpack2(ss[t][1], b0, b1);
+        ssum[t] = (a0 + b0) + (a1 + b1);
+      }
       const int par = gi & 1;
       mbar_wait(&m_empty[par], (((uint32_t)gi >> 1) & 1u) ^ 1u);
-#pragma unroll
       for (int t = 0; t < 4; ++t) {
         uint32_t bal = 0;
         if (t < T) {
@@ -266,30 +285,49 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           tc_fence_after();
           const int64_t r = r0 + (int64_t)t * 128 + row;
           const bool valid = r < r1;
-          const float scale = rms_scale(ss0[t] + ss1[t], p.inv_d, p.eps);
-          float acc = 0.f;
+          const float sq = t == 0 ? ssum[0] : t == 1 ? ssum[1] : t == 2 ? ssum[2] : ssum[3];
+          const float scale = rms_scale(sq, p.inv_d, p.eps);
+          const f32x2 scale2 = pack2(scale, scale);
+          const float nsl = -scale * 1.4426950408889634f;
+          const f32x2 nsl2 = pack2(nsl, nsl);
+          f32x2 acc2 = 0ull;
           const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(t * p.bp);
           for (int c0 = 0; c0 < p.b; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(taddr + (uint32_t)c0, v);
             tmem_ld_wait();
+            if (c0 + 32 <= p.b) {
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              const int j = c0 + jj;
-              if (j < p.b) {
-                const float a = __fmul_rn(__uint_as_float(v[jj]), scale);
-                acc = fmaf(sWup[j], silu_f32(a), acc);
+              for (int jj = 0; jj < 32; jj += 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(sWup + c0 + jj);
+                const f32x2 s01 = silu2_fast(pack2u(v[jj], v[jj + 1]), scale2, nsl2);
+                const f32x2 s23 = silu2_fast(pack2u(v[jj + 2], v[jj + 3]), scale2, nsl2);
+                acc2 = ffma2(pack2(w4.x, w4.y), s01, acc2);
+                acc2 = ffma2(pack2(w4.z, w4.w), s23, acc2);
+              }
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 32; jj += 2) {
+                if (c0 + jj < p.b) {
+                  const float w0 = sWup[c0 + jj];
+                  const float w1 = (c0 + jj + 1 < p.b) ? sWup[c0 + jj + 1] : 0.0f;
+                  const f32x2 s01 = silu2_fast(pack2u(v[jj], v[jj + 1]), scale2, nsl2);
+                  acc2 = ffma2(pack2(w0, w1), s01, acc2);
+                }
               }
             }
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&t_empty[t]);
-          const float score = score_from_logit(acc);
+          float lo, hi;
+          unpack2(acc2, lo, hi);
+          const float logit = lo + hi;
+          const float score = score_from_logit(logit);
           const bool ex = valid && (score > p.theta);
           if (valid) {
             if (p.scores) p.scores[r] = score;
-            if (p.logits) p.logits[r] = acc;
+            if (p.logits) p.logits[r] = logit;
             if (p.mask) p.mask[r] = ex ? 1 : 0;
             if (ex && p.exit_layers) p.exit_layers[gathered ? p.row_idx[r] : r] = p.layer;
           }
@@ -477,11 +515,16 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n32));
   static bool attr_set[64] = {false};
   if (!attr_set[dev & 63]) {
-    cudaFuncSetAttribute(route_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(route_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(route_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
     attr_set[dev & 63] = true;
   }
-  route_tc_kernel<<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h32, tm_w, tm_g4, p);
+  if (a.dtype == TIDE_BF16)
+    route_tc_kernel<true><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h32, tm_w, tm_g4, p);
+  else
+    route_tc_kernel<false><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h32, tm_w, tm_g4, p);
   return check_launch("route_tc_kernel");
 }
 

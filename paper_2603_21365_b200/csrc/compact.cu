@@ -147,7 +147,7 @@ int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const i
                    int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,
                    void* cont_rows, int64_t* counts, void* workspace, cudaStream_t stream) {
   const int64_t ntiles = (n + kCTile - 1) / kCTile;
-  if (ntiles > kMaxParts) return set_error(TIDE_ERR_UNSUPPORTED, "mask too long for one launch");
+  if (ntiles > kMaxParts / 2) return set_error(TIDE_ERR_UNSUPPORTED, "mask too long for one launch");
   CompactParams p{};
   p.mask = mask;
   p.n_host = n;

@@ -220,7 +220,7 @@ int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int64_t nblk = (a.n + kSR - 1) / kSR;
-  if (nblk > kMaxParts) return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
+  if (nblk > kMaxParts / 2) return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)sm_count(dev) * 8));
   switch (a.dtype) {
     case TIDE_F32: route_simt_kernel<float><<<grid, kSThreads, 0, stream>>>(p); break;

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -36,7 +37,7 @@
 
 namespace tide {
 
-constexpr int kThreadsTC = 224;
+constexpr int kThreadsTC = 352;  // 11 warps: producer, MMA, 2 x 4 epilogue, compaction
 constexpr int kMaxNA = 16;
 constexpr int kMaxNW = 4;
 constexpr int kASlotBytes = 128 * 128;  // 128 rows x 64 cols x 2 B
@@ -61,12 +62,23 @@ struct TcParams {
   int64_t* exit_layers;
   int64_t* counts;
   Workspace* ws;
+  unsigned long long* dbg;  // optional per-CTA timeline (globaltimer ns), 8 slots per CTA
+  uint32_t dbg_flags;       // experiments only: 1 = skip RMS reads, 2 = skip MMAs
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Groups are balanced in units of kGran rows (the smallest TMA box of the
+// ragged tail), so per-CTA work differs by at most kGran rows.
+constexpr int kGran = 16;
 __device__ __forceinline__ void group_range(int64_t g, int64_t n, int64_t n32, int64_t ng,
                                             int64_t& r0, int64_t& r1) {
-  r0 = (g * n32 / ng) * 32;
-  r1 = ((g + 1) * n32 / ng) * 32;
+  r0 = (g * n32 / ng) * kGran;
+  r1 = ((g + 1) * n32 / ng) * kGran;
   if (r1 > n) r1 = n;
 }
 
@@ -97,9 +109,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
-  const int64_t n32 = (n + 31) / 32;
+  const int64_t n32 = (n + kGran - 1) / kGran;  // number of kGran-row units
   const int64_t G = gridDim.x;
-  const int64_t cpg = (int64_t)p.tpg * 4;
+  const int64_t cpg = (int64_t)p.tpg * (128 / kGran);
   int64_t NG = n32 < G ? n32 : G;
   if ((n32 + cpg - 1) / cpg > NG) NG = (n32 + cpg - 1) / cpg;
   const uint32_t tag = launch_tag(p.ws);
@@ -116,14 +128,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
     for (int i = 0; i < p.na; ++i) {
       mbar_init(&a_full[i], 1);
-      mbar_init(&a_empty[i], 1 + 4);  // MMA commit + 4 sum-of-squares warps
+      mbar_init(&a_empty[i], 1 + 4);  // MMA commit + the 4 RMS warps owning the tile
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 4);
+      mbar_init(&t_empty[i], 4);  // the 4 epilogue warps owning the tile
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&m_full[i], 4);
+      mbar_init(&m_full[i], 8);
       mbar_init(&m_empty[i], 1);
     }
     fence_mbar_init();
@@ -137,12 +149,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  unsigned long long* dbg = p.dbg ? p.dbg + 24 * blockIdx.x : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
 
   if (warp == 0) {
     // ----------------------------------------------------------- producer
     const uint64_t pol_h = policy_evict_first();
     const uint64_t pol_w = policy_evict_last();
     int as = 0, aph = 0, wsl = 0, wph = 0;
+    long long pw_cyc = 0, p_begin = clock64();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
       group_range(g, n, n32, NG, r0, r1);
@@ -156,23 +171,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (lane == 0) {
         for (int kc = 0; kc < p.nk; ++kc) {
           mbar_wait(&w_empty[wsl], wph ^ 1);
-          mbar_arrive_expect_tx(&w_full[wsl], p.wslot);
-          tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
+          if (p.dbg_flags & 4u) {
+            mbar_arrive(&w_full[wsl]);
+          } else {
+            mbar_arrive_expect_tx(&w_full[wsl], p.wslot);
+            tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
+          }
           if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
           for (int t = 0; t < T; ++t) {
+            const long long q0 = clock64();
             mbar_wait(&a_empty[as], aph ^ 1);
+            pw_cyc += clock64() - q0;
             uint8_t* dst = sA + (size_t)as * kASlotBytes;
             const int64_t rb = r0 + (int64_t)t * 128;
             const int rows_in = (int)((r1 - rb) < 128 ? (r1 - rb) : 128);
-            if (!gathered) {
+            if (p.dbg_flags & 4u) {
+              mbar_arrive(&a_full[as]);
+            } else if (!gathered) {
               if (rows_in == 128) {
                 mbar_arrive_expect_tx(&a_full[as], kASlotBytes);
                 tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
               } else {
-                const int nb = (rows_in + 31) / 32;
-                mbar_arrive_expect_tx(&a_full[as], nb * 4096);
+                const int nb = (rows_in + kGran - 1) / kGran;
+                mbar_arrive_expect_tx(&a_full[as], nb * kGran * 128);
                 for (int s = 0; s < nb; ++s)
-                  tma_load_2d(dst + s * 4096, &tm_h32, &a_full[as], kc * 64, (int)(rb + 32 * s),
+                  tma_load_2d(dst + s * kGran * 128, &tm_h32, &a_full[as], kc * 64, (int)(rb + kGran * s),
                               pol_h);
               }
             } else {
@@ -188,47 +211,77 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
       }
     }
+    if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[18] = pw_cyc; dbg[19] = clock64() - p_begin; }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      int as = 0, aph = 0, wsl = 0, wph = 0;
-      uint32_t accph = 0;
-      for (int64_t g = blockIdx.x; g < NG; g += G) {
-        int64_t r0, r1;
-        group_range(g, n, n32, NG, r0, r1);
-        const int T = (int)((r1 - r0 + 127) / 128);
-        for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
-        tc_fence_after();
-        for (int kc = 0; kc < p.nk; ++kc) {
-          mbar_wait(&w_full[wsl], wph);
-          tc_fence_after();
-          const uint32_t wbase = smem_u32(sW + (size_t)wsl * p.wslot);
-          for (int t = 0; t < T; ++t) {
-            mbar_wait(&a_full[as], aph);
-            tc_fence_after();
-            const uint32_t abase = smem_u32(sA + (size_t)as * kASlotBytes);
-            const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
+    // The whole warp walks the loop (warp-uniform state -> uniform registers);
+    // one elected lane issues.  Descriptors are built once per slot and
+    // advanced by +2 (32 bytes >> 4) per K=16 step.
+    int as = 0, aph = 0, wsl = 0, wph = 0;
+    uint32_t accph = 0;
+    long long wait_cyc = 0, t_begin = clock64();
+    const uint64_t desc_hi = sw128_kmajor_desc(0);
+    for (int64_t g = blockIdx.x; g < NG; g += G) {
+      int64_t r0, r1;
+      group_range(g, n, n32, NG, r0, r1);
+      const int T = (int)((r1 - r0 + 127) / 128);
+      for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
+      tc_fence_after();
+      for (int kc = 0; kc < p.nk; ++kc) {
+        const long long w0 = clock64();
+        mbar_wait(&w_full[wsl], wph);
+        int slot[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc_mma_f16(dt, sw128_kmajor_desc(abase + 32 * k), sw128_kmajor_desc(wbase + 32 * k),
-                         p.idesc, (kc | k) != 0);
-            tc_commit(&a_empty[as]);
-            if (kc == p.nk - 1) tc_commit(&t_full[t]);
+        for (int t = 0; t < 4; ++t) {
+          if (t < T) {
+            slot[t] = as;
+            mbar_wait(&a_full[as], aph);
             if (++as == p.na) { as = 0; aph ^= 1; }
           }
-          tc_commit(&w_empty[wsl]);
-          if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
         }
-        accph ^= (1u << T) - 1u;
+        wait_cyc += clock64() - w0;
+        tc_fence_after();
+        const uint64_t bdesc = desc_hi | (uint64_t)((smem_u32(sW + (size_t)wsl * p.wslot) & 0x3FFFFu) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if (t < T) {
+              const uint64_t adesc =
+                  desc_hi | (uint64_t)((smem_u32(sA + (size_t)slot[t] * kASlotBytes) & 0x3FFFFu) >> 4);
+              const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (!(p.dbg_flags & 2u))
+                  tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if (t < T) {
+              tc_commit(&a_empty[slot[t]]);
+              if (kc == p.nk - 1) tc_commit(&t_full[t]);
+            }
+          }
+          tc_commit(&w_empty[wsl]);
+        }
+        __syncwarp();
+        if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
       }
+      accph ^= (1u << T) - 1u;
     }
-  } else if (warp <= 5) {
+    if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = clock64() - t_begin; }
+  } else if (warp <= 9) {
     // ----------------------------------------------------------- RMS + epilogue
+    // Two sets of 4 warps: set 0 (warps 2-5) owns tiles 0-1, set 1 (warps 6-9)
+    // tiles 2-3 — both the RMS reads of those tiles' A slots and their
+    // epilogues, so the post-stream tail is split across 8 warps.
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int wset = (warp - 2) >> 2;
     const int row = 32 * q + lane;
     const uint32_t swz = (uint32_t)(row & 7);
     int as = 0, aph = 0, gi = 0;
     uint32_t accph = 0;
+    long long sw_cyc = 0, s_begin = clock64();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
       group_range(g, n, n32, NG, r0, r1);
@@ -240,13 +293,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int kc = 0; kc < p.nk; ++kc) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          if (t < T) {
+          if (t < T && (t >> 1) != wset) {
+            if (++as == p.na) { as = 0; aph ^= 1; }
+          } else if (t < T) {
+            const long long s0 = clock64();
             mbar_wait(&a_full[as], aph);
+            sw_cyc += clock64() - s0;
             const uint8_t* rp = sA + (size_t)as * kASlotBytes + row * 128;
             uint4 u[8];
+            if (p.dbg_flags & 1u) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
+              for (int j = 0; j < 8; ++j) u[j] = make_uint4(0, 0, 0, 0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_empty[as]);
 #pragma unroll
@@ -268,6 +330,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         }
       }
+      if (dbg && warp == 2 && lane == 0) { dbg[2] = gtimer(); dbg[20] = sw_cyc; dbg[21] = clock64() - s_begin; }
       float ssum[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -278,11 +341,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       const int par = gi & 1;
       mbar_wait(&m_empty[par], (((uint32_t)gi >> 1) & 1u) ^ 1u);
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 2 * wset; t < 2 * wset + 2; ++t) {
         uint32_t bal = 0;
         if (t < T) {
           mbar_wait(&t_full[t], (accph >> t) & 1u);
           tc_fence_after();
+          if (dbg && warp == 2 && lane == 0) dbg[8 + 2 * t] = gtimer();
           const int64_t r = r0 + (int64_t)t * 128 + row;
           const bool valid = r < r1;
           const float sq = t == 0 ? ssum[0] : t == 1 ? ssum[1] : t == 2 ? ssum[2] : ssum[3];
@@ -319,6 +383,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
           tc_fence_before();
           __syncwarp();
+          if (dbg && warp == 2 && lane == 0) dbg[9 + 2 * t] = gtimer();
           if (lane == 0) mbar_arrive(&t_empty[t]);
           float lo, hi;
           unpack2(acc2, lo, hi);
@@ -337,6 +402,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       accph ^= (1u << T) - 1u;
       __syncwarp();
+      if (dbg && warp == 2 && lane == 0) dbg[3] = gtimer();
       if (lane == 0) mbar_arrive(&m_full[par]);
       ++gi;
     }
@@ -360,8 +426,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       const uint32_t excl_w = incl - cnt;
       const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+      if (dbg && lane == 0) dbg[4] = gtimer();
       if (need_scan) {
         const uint32_t E = lookback_exclusive(p.ws->status, tag, g, agg);
+        if (dbg && lane == 0) dbg[5] = gtimer();
         if (p.exit_idx || p.cont_idx) {
           const int nwords = (int)((r1 - r0 + 31) / 32);
           const uint32_t lt = (1u << lane) - 1u;
@@ -399,8 +467,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
   }
+  if (dbg && threadIdx.x == 0) {
+    dbg[6] = gtimer();
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    dbg[7] = smid;
+  }
   if (threadIdx.x == 0) launch_done(p.ws);
 }
+
+static unsigned long long* g_dbg = nullptr;
+}  // namespace tide
+extern "C" void tide_debug_timeline(void* buf) { tide::g_dbg = (unsigned long long*)buf; }
+namespace tide {
 
 // ---------------------------------------------------------------------------
 // host side
@@ -499,20 +578,27 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.exit_layers = a.exit_layers;
   p.counts = a.counts;
   p.ws = reinterpret_cast<Workspace*>(a.workspace);
+  p.dbg = g_dbg;
+  {
+    static const char* env = getenv("TIDE_DEBUG_FLAGS");
+    p.dbg_flags = env ? (uint32_t)atoi(env) : 0u;
+  }
 
   CUtensorMap tm_h128, tm_h32, tm_w, tm_g4;
   const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
   int rc;
   if ((rc = make_map(&tm_h128, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
-  if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 32))) return rc;
+  if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, kGran))) return rc;
   if ((rc = make_map(&tm_g4, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 1))) return rc;
   if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
 
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = sm_count(dev);
-  const int64_t n32 = (a.n + 31) / 32;
+  const int64_t n32 = (a.n + kGran - 1) / kGran;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n32));
+  if ((n32 + tpg * (128 / kGran) - 1) / (tpg * (128 / kGran)) > kMaxParts / 2)
+    return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
   static bool attr_set[64] = {false};
   if (!attr_set[dev & 63]) {
     cudaFuncSetAttribute(route_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,141 @@
+"""Secondary timings for BASELINE.json configs 1-5 (bench.py --extra).
+
+Each entry: device time (CUDA events on the launching stream, after warm-up)
+of the B200 path for that config, with the algorithmic bytes it must move and
+the resulting GB/s.  Synthetic inputs (torch cuda generator), random routers
+N(0,1)*scale.  Not part of the driver's headline line.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import paper_2603_21365_b200 as P
+from oracle import tide_oracle as O
+
+
+def _time(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def _case(L, d, n, dtype, seed, scale, b=128):
+    g = np.random.Generator(np.random.PCG64(seed))
+    ckpts = O.checkpoint_layers(L, 4)
+    routers = {k: O.make_router(d, b, k, g, scale=scale) for k in ckpts}
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    states = [None] * (L + 1)
+    for k in list(ckpts) + [L - 1]:
+        states[k + 1] = torch.randn((n, d), generator=gen, device="cuda").to(dtype)
+    for i in range(L + 1):
+        if states[i] is None:
+            states[i] = states[L]
+    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L)
+    return ckpts, states, bank
+
+
+def config2(theta=0.5):
+    ckpts, states, bank = _case(32, 4096, 4096, torch.bfloat16, 2, 0.1)
+    cfg = P.RuntimeConfig(exit_threshold=theta)
+    exits = P.select_exits(states, bank, cfg)
+    ms = _time(lambda: P.select_exits(states, bank, cfg))
+    # peeled bytes: every remaining row at every checkpoint
+    e = exits.cpu().numpy()
+    remaining, peeled = 4096, 0
+    for k in ckpts:
+        peeled += remaining * (4096 * 2 + 21)
+        remaining -= int((e == k).sum())
+    peeled += len(ckpts) * (128 * 4096 * 2 + 512)
+    return {"config": "2: DeepSeek-8B prefill, L=32 (8 ckpts), d=4096, 4,096 tok, bf16, "
+                      f"per-token theta={theta}",
+            "ms": ms, "tokens_per_s": 4096 / (ms / 1e3), "peeled_bytes": peeled,
+            "gbs": peeled / (ms / 1e3) / 1e9, "exit_rate": float((e >= 0).mean()),
+            "launches": len(ckpts)}
+
+
+def config3(mode=P.PER_TOKEN, dtype=torch.bfloat16):
+    ckpts, states, bank = _case(36, 4096, 8, dtype, 3, 0.3)
+    cfg = P.RuntimeConfig(exit_threshold=0.5, mode=mode)
+    ms = _time(lambda: P.select_exits(states, bank, cfg), reps=50)
+    byts = len(ckpts) * (8 * 4096 * 2 + 128 * 4096 * 2)
+    return {"config": f"3: Qwen3-8B decode, L=36 (9 ckpts), d=4096, 8 rows, {dtype}, {mode}",
+            "us_per_step": ms * 1e3, "bytes": byts, "gbs": byts / (ms / 1e3) / 1e9,
+            "launches": 1}
+
+
+def config4(n=1_024_000, d=4096, C=8):
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(4)
+    fin = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
+    cks = {}
+    for i in range(C + 1):
+        t = fin if i == C else torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
+        for r0 in range(0, n, 131072):
+            r1 = min(n, r0 + 131072)
+            t[r0:r1] = torch.randn((r1 - r0, d), generator=gen, device="cuda").to(torch.bfloat16)
+        if i < C:
+            cks[3 + 4 * i] = t
+    ms = _time(lambda: P.label_tensors(cks, fin, 0.98, labels_dtype="u8"), reps=3, warm=1)
+    byts = n * (C + 1) * d * 2 + n * C * 5
+    out = {"config": f"4: calibration labeller, {n:,} tok x d={d} bf16, {C} ckpts + final",
+           "ms": ms, "bytes": byts, "gbs": byts / (ms / 1e3) / 1e9}
+    del fin, cks
+    torch.cuda.empty_cache()
+    return out
+
+
+def config5():
+    ckpts, states, bank = _case(80, 8192, 8192, torch.bfloat16, 5, 0.06)
+    cfg = P.RuntimeConfig(exit_threshold=0.7)
+    exits = P.select_exits(states, bank, cfg)
+    ms = _time(lambda: P.select_exits(states, bank, cfg))
+    e = exits.cpu().numpy()
+    remaining, peeled = 8192, 0
+    for k in ckpts:
+        peeled += remaining * (8192 * 2 + 21)
+        remaining -= int((e == k).sum())
+    return {"config": "5: 70B prefill shard, L=80 (20 ckpts), d=8192, 8,192 tok/GPU, bf16",
+            "ms": ms, "tokens_per_s": 8192 / (ms / 1e3), "peeled_bytes": peeled,
+            "gbs": peeled / (ms / 1e3) / 1e9, "exit_rate": float((e >= 0).mean()),
+            "launches": len(ckpts)}
+
+
+def config1():
+    g = np.random.Generator(np.random.PCG64(42))
+    ckpts = O.checkpoint_layers(12, 4)
+    routers = {k: O.make_router(768, 128, k, g) for k in ckpts}
+    states = [torch.from_numpy(g.standard_normal((2048, 768), dtype=np.float32)).cuda()
+              for _ in range(13)]
+    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=12)
+    cfg = P.RuntimeConfig(exit_threshold=0.5)
+    ms = _time(lambda: P.select_exits(states, bank, cfg))
+    return {"config": "1: GPT-2-small shape, L=12 (3 ckpts), d=768, 2,048 tok, fp32 (CUDA-core "
+                      "path, f32 products)", "ms": ms, "tokens_per_s": 2048 / (ms / 1e3)}
+
+
+def run_extra(dev=None):
+    out = []
+    for fn in (config1, config2, config3,
+               lambda: config3(P.BATCH_UNANIMOUS), lambda: config3(dtype=torch.float16),
+               config5, config4):
+        try:
+            out.append(fn())
+        except Exception as e:  # report, do not hide
+            out.append({"error": repr(e)})
+    return out
+
+
+if __name__ == "__main__":
+    import json
+    for r in run_extra():
+        print(json.dumps(r))

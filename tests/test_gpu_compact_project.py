@@ -1,0 +1,160 @@
+"""GPU parity: standalone stable compaction (batch_compact) and exit
+scatter / projection — restates pkg/tests/test_router_ops.py:109-231 and
+test_acceptance.py #7 against the kernels; bit-exact vs the reference."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_21365_b200 as P
+from paper_2603_21365_b200 import _device as D
+from paper_2603_21365_b200 import _native as N
+from oracle import tide_oracle as O
+from tests.gpu_helpers import need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def naive_partition(mask):
+    cont = [i for i in range(len(mask)) if not mask[i]]
+    exi = [i for i in range(len(mask)) if mask[i]]
+    return cont, exi
+
+
+def test_golden_masks_bit_exact(golden_compact):
+    need_gpu()
+    g = golden_compact
+    for i in range(int(g["n_masks"][0])):
+        mask = g[f"m{i}__mask"]
+        h = np.arange(mask.shape[0] * 3, dtype=np.float32).reshape(-1, 3)
+        for strategy in ("small", "prefix", "auto"):
+            r = P.batch_compact(h, mask, strategy=strategy)
+            key = "small" if strategy == "small" else "prefix"
+            np.testing.assert_array_equal(r.exiting_indices, g[f"m{i}__{key}__exit"])
+            np.testing.assert_array_equal(r.continuing_indices, g[f"m{i}__{key}__cont"])
+            np.testing.assert_array_equal(r.exiting, h[r.exiting_indices])
+            np.testing.assert_array_equal(r.continuing, h[r.continuing_indices])
+
+
+def test_acceptance_7_exhaustive_and_random():
+    """test_acceptance.py:167-210: all 256 masks at batch 8, 200 random at 1000."""
+    need_gpu()
+    rng = np.random.Generator(np.random.PCG64(707))
+    rows8 = rng.standard_normal((8, 5), dtype=np.float32)
+    for bits in range(256):
+        mask = np.array([(bits >> i) & 1 == 1 for i in range(8)])
+        r = P.batch_compact(rows8, mask)
+        c, e = naive_partition(mask)
+        np.testing.assert_array_equal(r.exiting_indices, e)
+        np.testing.assert_array_equal(r.continuing_indices, c)
+        rebuilt = np.zeros_like(rows8)
+        rebuilt[np.asarray(c, np.int64)] = r.continuing
+        P.exit_scatter(r.exiting, r.exiting_indices, rebuilt)
+        np.testing.assert_array_equal(rebuilt, rows8)
+    rows = torch.from_numpy(rng.standard_normal((1000, 7), dtype=np.float32)).cuda()
+    for _ in range(200):
+        mask = rng.random(1000) < rng.random()
+        r = P.batch_compact(rows, torch.from_numpy(mask).cuda())
+        c, e = naive_partition(mask)
+        np.testing.assert_array_equal(r.exiting_indices.cpu().numpy(), e)
+        np.testing.assert_array_equal(r.continuing_indices.cpu().numpy(), c)
+        np.testing.assert_array_equal(r.exiting.cpu().numpy(), rows.cpu().numpy()[e])
+
+
+@pytest.mark.parametrize("n", [0, 1, 2047, 2048, 2049, 100_000, 1_000_003])
+def test_large_and_ragged_masks(n):
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(n + 5))
+    mask = g.random(n) < 0.37
+    dm = torch.from_numpy(mask.astype(np.uint8)).cuda()
+    ex = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    co = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    counts = torch.full((2,), -1, dtype=torch.int64, device="cuda")
+    N.check(N.load().tide_compact(dm.data_ptr() if n else 0, n, None, None, 0, None, 0, 0, 0,
+                                  ex.data_ptr(), co.data_ptr(), None, None, counts.data_ptr(),
+                                  D.workspace().data_ptr(), D.stream_handle()), "tide_compact")
+    e, c = O.compact_indices(mask)
+    assert int(counts[0]) == len(e) and int(counts[1]) == len(c)
+    np.testing.assert_array_equal(ex[: len(e)].cpu().numpy(), e)
+    np.testing.assert_array_equal(co[: len(c)].cpu().numpy(), c)
+
+
+def test_all_and_none_exit(rng):
+    need_gpu()
+    h = rng.standard_normal((9, 4), dtype=np.float32)
+    all_out = P.batch_compact(h, np.ones(9, bool))
+    assert all_out.continuing.shape == (0, 4)
+    np.testing.assert_array_equal(all_out.exiting, h)
+    none_out = P.batch_compact(h, np.zeros(9, bool))
+    assert none_out.exiting.shape == (0, 4)
+    np.testing.assert_array_equal(none_out.continuing, h)
+
+
+def test_compact_errors_match_reference():
+    need_gpu()
+    with pytest.raises(ValueError, match="mask"):
+        P.batch_compact(np.zeros((4, 2), np.float32), np.zeros(3, bool))
+    with pytest.raises(ValueError, match="strategy"):
+        P.batch_compact(np.zeros((2, 2), np.float32), np.zeros(2, bool), strategy="warp")
+
+
+def test_bf16_rows_gather_bit_exact():
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(31))
+    h = torch.randn((3000, 4096), device="cuda").to(torch.bfloat16)
+    mask = g.random(3000) < 0.5
+    r = P.batch_compact(h, torch.from_numpy(mask).cuda())
+    e, c = O.compact_indices(mask)
+    assert torch.equal(r.exiting, h[torch.from_numpy(e).cuda()])
+    assert torch.equal(r.continuing, h[torch.from_numpy(c).cuda()])
+
+
+def test_projection_golden(golden_projection):
+    need_gpu()
+    g = golden_projection
+    out = np.full((20, 64), -1.0, np.float32)
+    P.exit_projection(g["rows"], g["gain"], O.DEFAULT_EPS, g["positions"], out)
+    np.testing.assert_allclose(out, g["out"], rtol=2e-6, atol=1e-6)
+    out2 = np.full((20, 64), -1.0, np.float32)
+    P.exit_projection(g["rows"], None, O.DEFAULT_EPS, g["positions"], out2)
+    np.testing.assert_allclose(out2, g["out_nogain"], rtol=2e-6, atol=1e-6)
+    # untouched rows preserved exactly
+    untouched = np.setdiff1d(np.arange(20), g["positions"])
+    assert np.all(out[untouched] == -1.0)
+
+
+def test_scatter_roundtrip_and_validation(rng):
+    need_gpu()
+    h = rng.standard_normal((30, 8), dtype=np.float32)
+    mask = rng.integers(0, 2, size=30).astype(bool)
+    res = P.batch_compact(h, mask)
+    out = np.zeros_like(h)
+    P.exit_scatter(res.exiting, res.exiting_indices, out)
+    P.exit_scatter(res.continuing, res.continuing_indices, out)
+    np.testing.assert_array_equal(out, h)
+    out = np.zeros((5, 2), np.float32)
+    with pytest.raises(ValueError, match="strictly increasing"):
+        P.exit_scatter(np.ones((2, 2), np.float32), [3, 1], out)
+    with pytest.raises(ValueError, match="strictly increasing"):
+        P.exit_scatter(np.ones((2, 2), np.float32), [2, 2], out)
+    with pytest.raises(ValueError, match="range"):
+        P.exit_scatter(np.ones((2, 2), np.float32), [1, 3], np.zeros((3, 2), np.float32))
+    with pytest.raises(ValueError, match="width"):
+        P.exit_scatter(np.ones((1, 2), np.float32), [0], np.zeros((3, 4), np.float32))
+    keep = np.full((3, 2), 7.0, np.float32)
+    P.exit_scatter(np.zeros((0, 2), np.float32), np.zeros(0, np.int64), keep)
+    assert np.all(keep == 7.0)
+
+
+def test_projection_bf16_rows_device():
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(41))
+    rows = O.round_to(g.standard_normal((257, 4096), dtype=np.float32) * 3, "bf16")
+    gain = g.standard_normal(4096, dtype=np.float32)
+    pos = np.sort(g.choice(1000, 257, replace=False)).astype(np.int64)
+    out = torch.zeros((1000, 4096), dtype=torch.float32, device="cuda")
+    P.exit_projection(torch.from_numpy(rows).cuda().to(torch.bfloat16),
+                      torch.from_numpy(gain).cuda(), 1e-6, torch.from_numpy(pos).cuda(), out)
+    want = np.zeros((1000, 4096), np.float32)
+    O.exit_projection(rows, gain, 1e-6, pos, want)
+    np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-5, atol=1e-5)

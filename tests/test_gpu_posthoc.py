@@ -1,0 +1,215 @@
+"""GPU parity: posthoc_select (per-token peeling chain, batch-unanimous, decode
+path) vs the reference golden exit maps / logits — restates
+pkg/tests/test_runtime.py:42-147 against the device path, plus configs 2, 3
+and 5 shapes against the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_21365_b200 as P
+from oracle import tide_oracle as O
+from tests.golden.cases import (bank_from_golden, digest, posthoc_cases, posthoc_states,
+                                rigged_router_arrays, stored_digest)
+from tests.gpu_helpers import RTOL, excused_rows, need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _bank(g, bname):
+    ckpts, eps, ws = bank_from_golden(g, bname)
+    return P.make_bank(ws, num_layers=12, interval=4, eps=eps), ckpts, eps, ws
+
+
+def _head(g):
+    return P.OutputHead(12, 64, g["final_norm"], g["lm_head"])
+
+
+def test_golden_exit_maps_and_logits(golden_posthoc):
+    need_gpu()
+    g = golden_posthoc
+    head = _head(g)
+    banks = {b: _bank(g, b) for b in ("rigged", "trained")}
+    cache = {}
+    n_checked = 0
+    for idx, (seed, n, zero_row, bname, theta, mode, k_min) in enumerate(posthoc_cases(g)):
+        key = (seed, n, zero_row)
+        if key not in cache:
+            cache[key] = posthoc_states(seed, n, zero_row)
+        states = cache[key]
+        assert digest(*states) == stored_digest(g, f"c{idx}__digest")
+        bank, ckpts, eps, ws = banks[bname]
+        cfg = P.RuntimeConfig(exit_threshold=theta, mode=mode, k_min=k_min)
+        logits, exits = P.posthoc_select(head, states, bank, cfg)
+        want = g[f"c{idx}__exits"]
+        routers = {k: O.OracleRouter(k, *ws[k]) for k in ckpts}
+        exc = excused_rows(states, routers, theta, "f32", k_min)
+        if mode == P.BATCH_UNANIMOUS and exc.any():
+            exc[:] = True  # one excused row can flip the unanimous decision for all
+        assert np.all((exits == want) | exc), (idx, exits, want)
+        if f"c{idx}__logits" in g.files and not exc.any():
+            np.testing.assert_allclose(logits, g[f"c{idx}__logits"], atol=1e-5, rtol=0)
+        n_checked += 1
+    assert n_checked == 200
+
+
+def test_reference_runtime_semantics(golden_posthoc):
+    """pkg/tests/test_runtime.py:52-137 on the device path."""
+    need_gpu()
+    g = golden_posthoc
+    head = _head(g)
+    rigged, _, _, _ = _bank(g, "rigged")
+    rng = np.random.Generator(np.random.PCG64(1234))
+    states = [rng.standard_normal((6, 64), dtype=np.float32) for _ in range(13)]
+    base = O.lm_head_from_hidden(g["final_norm"], g["lm_head"], states[-1])
+    for mode in P.MODES:
+        logits, exits = P.posthoc_select(head, states, rigged,
+                                         P.RuntimeConfig(exit_threshold=1.0, mode=mode))
+        assert np.all(exits == P.NO_EXIT)
+        np.testing.assert_allclose(logits, base, atol=1e-5)
+        logits, exits = P.posthoc_select(head, states, rigged,
+                                         P.RuntimeConfig(exit_threshold=0.5, mode=mode))
+        assert np.all(exits == 7)
+        np.testing.assert_allclose(
+            logits, O.lm_head_from_hidden(g["final_norm"], g["lm_head"], states[8]), atol=1e-5)
+    _, exits = P.posthoc_select(head, states, rigged, P.RuntimeConfig(exit_threshold=0.5, k_min=8))
+    assert np.all(exits == P.NO_EXIT)
+    states[8][2] = 0.0
+    _, per_token = P.posthoc_select(head, states, rigged, P.RuntimeConfig(exit_threshold=0.5))
+    want = np.full(6, 7)
+    want[2] = P.NO_EXIT
+    np.testing.assert_array_equal(per_token, want)
+    _, unanimous = P.posthoc_select(head, states, rigged,
+                                    P.RuntimeConfig(exit_threshold=0.5, mode=P.BATCH_UNANIMOUS))
+    assert np.all(unanimous == P.NO_EXIT)
+    logits, exits = P.posthoc_select(head, states, None, P.RuntimeConfig())
+    assert np.all(exits == P.NO_EXIT)
+    with pytest.raises(ValueError, match="hidden states"):
+        P.posthoc_select(head, states[:-1], rigged, P.RuntimeConfig())
+    with pytest.raises(ValueError, match="width"):
+        P.posthoc_select(head, [s[:, :32] for s in states], rigged, P.RuntimeConfig())
+
+
+def test_reference_bank_object_is_accepted(golden_posthoc):
+    """Duck-typed drop-in: an object with the reference RouterBank's fields."""
+    need_gpu()
+    g = golden_posthoc
+    ours, ckpts, eps, ws = _bank(g, "trained")
+
+    class RefLikeBank:  # fields of ee/calibration.py:351-382
+        pass
+
+    b = RefLikeBank()
+    for f in ("hidden_dim", "bottleneck", "interval", "tau", "eps", "num_layers", "routers"):
+        setattr(b, f, getattr(ours, f))
+    b.checkpoints = ours.checkpoints
+    states = posthoc_states(1236, 300)
+    cfg = P.RuntimeConfig(exit_threshold=0.5)
+    _, e1 = P.posthoc_select(_head(g), states, ours, cfg)
+    _, e2 = P.posthoc_select(_head(g), states, b, cfg)
+    np.testing.assert_array_equal(e1, e2)
+
+
+def _big_case(L, d, n, dtype, seed, scale=0.1):
+    """Synthetic capture + bank at a BASELINE config shape (device tensors)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    ckpts = O.checkpoint_layers(L, 4)
+    routers = {k: O.make_router(d, 128, k, g, scale=scale) for k in ckpts}
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16}[dtype]
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    states = [None] * (L + 1)
+    for k in list(ckpts) + [L - 1]:
+        states[k + 1] = torch.randn((n, d), generator=gen, device="cuda").to(tdt)
+    for i in range(L + 1):
+        if states[i] is None:
+            states[i] = states[L]  # never read by the exit path
+    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L)
+    head = P.OutputHead(L, d, np.ones(d, np.float32),
+                        (g.standard_normal((256, d)) * 0.02).astype(np.float32))
+    return ckpts, routers, states, bank, head
+
+
+@pytest.mark.parametrize("theta", [0.5, 0.85, 1.0])
+@pytest.mark.parametrize("mode", [P.PER_TOKEN, P.BATCH_UNANIMOUS])
+def test_config2_prefill_shape(theta, mode):
+    """DeepSeek-8B shape: L=32 (8 checkpoints), d=4096, 4,096 tokens, bf16."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(32, 4096, 4096, "bf16", 2)
+    cfg = P.RuntimeConfig(exit_threshold=theta, mode=mode)
+    logits, exits = P.posthoc_select(head, states, bank, cfg)
+    host = {k + 1: states[k + 1].float().cpu().numpy() for k in ckpts}
+    scores, exc = {}, np.zeros(4096, bool)
+    for k in ckpts:
+        s, t, m = O.route_logits(host[k + 1], routers[k])
+        scores[k] = s
+        if theta < 1.0:
+            exc |= np.abs(t - O.logit_of(theta)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
+    want = O.first_exit_from_scores(scores, theta, 0, mode)
+    got = exits.cpu().numpy()
+    if mode == P.BATCH_UNANIMOUS and exc.any():
+        exc[:] = True
+    assert np.all((got == want) | exc)
+    if theta == 1.0:
+        assert np.all(got == P.NO_EXIT)
+    # logits: final-norm of the chosen layer's row through the LM head
+    fin = states[32].float().cpu().numpy()
+    rows = np.stack([host[int(k) + 1][i] if k >= 0 else fin[i] for i, k in enumerate(got)])
+    ref = O.lm_head_from_hidden(np.ones(4096, np.float32), head.lm_head, rows)
+    np.testing.assert_allclose(logits.cpu().numpy(), ref, atol=2e-4, rtol=1e-4)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("mode", [P.PER_TOKEN, P.BATCH_UNANIMOUS])
+@pytest.mark.parametrize("n", [1, 8, 16])
+def test_config3_decode_step(dtype, mode, n):
+    """Qwen3-8B shape decode: L=36 (9 checkpoints), d=4096, <=16 rows, one launch."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(36, 4096, n, dtype, 3, scale=0.3)
+    for theta in (0.5, 0.85, 1.0):
+        cfg = P.RuntimeConfig(exit_threshold=theta, mode=mode)
+        exits = P.select_exits(states, bank, cfg).cpu().numpy()
+        scores, exc = {}, np.zeros(n, bool)
+        for k in ckpts:
+            s, t, m = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
+            scores[k] = s
+            if theta < 1.0:
+                exc |= np.abs(t - O.logit_of(theta)) <= RTOL[dtype] * np.maximum(np.abs(t), m)
+        want = O.first_exit_from_scores(scores, theta, 0, mode)
+        if mode == P.BATCH_UNANIMOUS and exc.any():
+            exc[:] = True
+        assert np.all((exits == want) | exc), (theta, exits, want)
+
+
+def test_config5_shard_shape_peeling_chain():
+    """70B shape, one 8,192-token shard: d=8192, 20 checkpoints, bf16."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(80, 8192, 8192, "bf16", 5, scale=0.06)
+    exits = P.select_exits(states, bank, P.RuntimeConfig(exit_threshold=0.7)).cpu().numpy()
+    scores, exc = {}, np.zeros(2048, bool)
+    for k in ckpts:
+        s, t, m = O.route_logits(states[k + 1][:2048].float().cpu().numpy(), routers[k])
+        scores[k] = s
+        exc |= np.abs(t - O.logit_of(0.7)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
+    want = O.first_exit_from_scores(scores, 0.7)
+    assert np.all((exits[:2048] == want) | exc)
+    assert (exits >= 0).mean() > 0.05  # the chain actually peels rows
+
+
+def test_rigged_hot_bf16_device_exact():
+    """Rigged routers saturate to exactly 1.0 / 0.0 on the tensor-core path too."""
+    need_gpu()
+    d = 64
+    L = 12
+    routers = {k: rigged_router_arrays(d, hot=(k == 7)) for k in (3, 7, 11)}
+    bank = P.make_bank(routers, num_layers=L)
+    g = np.random.Generator(np.random.PCG64(9))
+    states = [torch.from_numpy(O.round_to(g.standard_normal((500, d), dtype=np.float32), "bf16"))
+              .cuda().to(torch.bfloat16) for _ in range(L + 1)]
+    states[8][17] = 0.0  # zero row scores exactly 0.5 at layer 7 -> never exits
+    head = P.OutputHead(L, d, np.ones(d, np.float32), np.eye(d, dtype=np.float32))
+    _, exits = P.posthoc_select(head, states, bank, P.RuntimeConfig(exit_threshold=0.5))
+    e = exits.cpu().numpy()
+    assert e[17] == P.NO_EXIT and np.all(np.delete(e, 17) == 7)
+    _, exits = P.posthoc_select(head, states, bank, P.RuntimeConfig(exit_threshold=1.0))
+    assert np.all(exits.cpu().numpy() == P.NO_EXIT)

@@ -127,7 +127,7 @@ def ncu_traffic(kernel: str):
     if os.path.exists(p):
         with open(p) as fh:
             d = json.load(fh)
-        return d.get(kernel)
+        return d.get(kernel, d.get(kernel + "_bf16"))
     return None
 
 

@@ -4,6 +4,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -113,7 +114,14 @@ int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool aligned = ((reinterpret_cast<uintptr_t>(h) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(w_down) & 15) == 0) && (ld_h % 8 == 0);
-  if (route_tc_supported(dtype, d, b) && aligned) return route_tc_launch(a, s);
+  if (route_tc_supported(dtype, d, b) && aligned) {
+    // Single-CTA kernel by default; TIDE_K1_PAIR=1 selects the CTA-pair
+    // (cta_group::2) variant (measured slower so far: DESIGN.md §3).
+    static const char* pair = getenv("TIDE_K1_PAIR");
+    const int npad = (b + 15) / 16 * 16;
+    if (pair && pair[0] == '1' && (npad / 2) % 8 == 0) return route_tc2_launch(a, s);
+    return route_tc_launch(a, s);
+  }
   return route_simt_launch(a, s);
 }
 

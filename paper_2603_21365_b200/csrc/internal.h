@@ -1,6 +1,7 @@
 // Host-side internals shared by the launchers and the C ABI (capi.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -39,6 +40,10 @@ int check_launch(const char* what);
 int sm_count(int device);
 
 bool route_tc_supported(int dtype, int d, int b);
+int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, int64_t rows,
+             int64_t ld_elems, int box_cols, int box_rows);
+extern unsigned long long* g_dbg;
+int route_tc2_launch(const RouteArgs& a, cudaStream_t stream);
 int route_tc_launch(const RouteArgs& a, cudaStream_t stream);
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream);
 int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,

@@ -63,6 +63,7 @@ struct TcParams {
   int64_t* counts;
   Workspace* ws;
   unsigned long long* dbg;  // optional per-CTA timeline (globaltimer ns), 8 slots per CTA
+  int32_t prefetch;
   uint32_t dbg_flags;       // experiments only: 1 = skip RMS reads, 2 = skip MMAs
 };
 
@@ -85,6 +86,8 @@ __device__ __forceinline__ void group_range(int64_t g, int64_t n, int64_t n32, i
 template <bool kBF16>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     route_tc_kernel(const __grid_constant__ CUtensorMap tm_h128,
+                    const __grid_constant__ CUtensorMap tm_h64,
+                    const __grid_constant__ CUtensorMap tm_h32b,
                     const __grid_constant__ CUtensorMap tm_h32,
                     const __grid_constant__ CUtensorMap tm_w,
                     const __grid_constant__ CUtensorMap tm_g4, const __grid_constant__ TcParams p) {
@@ -154,8 +157,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   if (warp == 0) {
     // ----------------------------------------------------------- producer
-    const uint64_t pol_h = policy_evict_first();
-    const uint64_t pol_w = policy_evict_last();
+    const uint64_t pol_h = (p.dbg_flags & 16u) ? 0x1000000000000000ull : policy_evict_first();
+    const uint64_t pol_w = (p.dbg_flags & 16u) ? 0x1000000000000000ull : policy_evict_last();
     int as = 0, aph = 0, wsl = 0, wph = 0;
     long long pw_cyc = 0, p_begin = clock64();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
@@ -169,7 +172,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         __syncwarp();
       }
       if (lane == 0) {
+        const int pd = p.prefetch;  // k-chunks of L2 prefetch ahead of the smem ring
+        if (!gathered && pd > 0)
+          for (int kc = 0; kc < pd && kc < p.nk; ++kc)
+            for (int t = 0; t < T; ++t) tma_prefetch_2d(&tm_h128, kc * 64, (int)(r0 + 128 * t));
         for (int kc = 0; kc < p.nk; ++kc) {
+          if (!gathered && pd > 0 && kc + pd < p.nk)
+            for (int t = 0; t < T; ++t)
+              tma_prefetch_2d(&tm_h128, (kc + pd) * 64, (int)(r0 + 128 * t));
           mbar_wait(&w_empty[wsl], wph ^ 1);
           if (p.dbg_flags & 4u) {
             mbar_arrive(&w_full[wsl]);
@@ -188,15 +198,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (p.dbg_flags & 4u) {
               mbar_arrive(&a_full[as]);
             } else if (!gathered) {
-              if (rows_in == 128) {
+              if (rows_in == 128 || (p.dbg_flags & 32u)) {
                 mbar_arrive_expect_tx(&a_full[as], kASlotBytes);
                 tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
               } else {
-                const int nb = (rows_in + kGran - 1) / kGran;
-                mbar_arrive_expect_tx(&a_full[as], nb * kGran * 128);
-                for (int s = 0; s < nb; ++s)
-                  tma_load_2d(dst + s * kGran * 128, &tm_h32, &a_full[as], kc * 64, (int)(rb + kGran * s),
-                              pol_h);
+                // ragged tail: greedy 64/32/16-row boxes (16-row boxes stream poorly)
+                const int rr = (rows_in + kGran - 1) / kGran * kGran;
+                mbar_arrive_expect_tx(&a_full[as], (uint32_t)(rr * 128));
+                int off = 0;
+                if (rr - off >= 64) {
+                  tma_load_2d(dst, &tm_h64, &a_full[as], kc * 64, (int)rb, pol_h);
+                  off += 64;
+                }
+                if (rr - off >= 32) {
+                  tma_load_2d(dst + off * 128, &tm_h32b, &a_full[as], kc * 64, (int)(rb + off), pol_h);
+                  off += 32;
+                }
+                if (rr - off >= 16) {
+                  tma_load_2d(dst + off * 128, &tm_h32, &a_full[as], kc * 64, (int)(rb + off), pol_h);
+                  off += 16;
+                }
               }
             } else {
               const int ng4 = (rows_in + 3) / 4;
@@ -230,39 +251,64 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int kc = 0; kc < p.nk; ++kc) {
         const long long w0 = clock64();
         mbar_wait(&w_full[wsl], wph);
-        int slot[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          if (t < T) {
-            slot[t] = as;
-            mbar_wait(&a_full[as], aph);
-            if (++as == p.na) { as = 0; aph ^= 1; }
-          }
-        }
         wait_cyc += clock64() - w0;
-        tc_fence_after();
         const uint64_t bdesc = desc_hi | (uint64_t)((smem_u32(sW + (size_t)wsl * p.wslot) & 0x3FFFFu) >> 4);
-        if (elect_one()) {
+        if (p.dbg_flags & 64u) {
+          // batched: wait every tile's slot, one fence, all MMAs, then commits
+          int slot[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             if (t < T) {
+              slot[t] = as;
+              mbar_wait(&a_full[as], aph);
+              if (++as == p.na) { as = 0; aph ^= 1; }
+            }
+          }
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              if (t < T) {
+                const uint64_t adesc =
+                    desc_hi | (uint64_t)((smem_u32(sA + (size_t)slot[t] * kASlotBytes) & 0x3FFFFu) >> 4);
+                const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  if (!(p.dbg_flags & 2u))
+                    tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+              }
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              if (t < T) {
+                tc_commit(&a_empty[slot[t]]);
+                if (kc == p.nk - 1) tc_commit(&t_full[t]);
+              }
+            }
+            tc_commit(&w_empty[wsl]);
+          }
+        } else {
+          // per tile: its slot is released as soon as ITS 4 MMAs retire
+          for (int t = 0; t < T; ++t) {
+            const long long w1 = clock64();
+            mbar_wait(&a_full[as], aph);
+            wait_cyc += clock64() - w1;
+            tc_fence_after();
+            if (elect_one()) {
               const uint64_t adesc =
-                  desc_hi | (uint64_t)((smem_u32(sA + (size_t)slot[t] * kASlotBytes) & 0x3FFFFu) >> 4);
+                  desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * kASlotBytes) & 0x3FFFFu) >> 4);
               const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 if (!(p.dbg_flags & 2u))
                   tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            if (t < T) {
-              tc_commit(&a_empty[slot[t]]);
+              tc_commit(&a_empty[as]);
               if (kc == p.nk - 1) tc_commit(&t_full[t]);
             }
+            __syncwarp();
+            if (++as == p.na) { as = 0; aph ^= 1; }
           }
-          tc_commit(&w_empty[wsl]);
+          if (elect_one()) tc_commit(&w_empty[wsl]);
         }
         __syncwarp();
         if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
@@ -476,7 +522,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (threadIdx.x == 0) launch_done(p.ws);
 }
 
-static unsigned long long* g_dbg = nullptr;
+unsigned long long* g_dbg = nullptr;
 }  // namespace tide
 extern "C" void tide_debug_timeline(void* buf) { tide::g_dbg = (unsigned long long*)buf; }
 namespace tide {
@@ -489,7 +535,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static EncodeTiledFn encode_fn() {
+EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -503,8 +549,44 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-static int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, int64_t rows,
-                    int64_t ld_elems, int box_cols, int box_rows) {
+// Tensor maps are encoded on the host per (pointer, shape, box); a small cache
+// keeps repeated launches over the same buffers (bench loops, the posthoc chain
+// over a persistent capture) from paying the driver encode every time.
+namespace {
+struct MapKey {
+  const void* base;
+  int dtype;
+  int64_t cols, rows, ld;
+  int bc, br;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && dtype == o.dtype && cols == o.cols && rows == o.rows && ld == o.ld &&
+           bc == o.bc && br == o.br;
+  }
+};
+constexpr int kMapCache = 128;
+struct MapEntry {
+  MapKey key;
+  CUtensorMap map;
+  uint64_t stamp;
+  bool used;
+};
+MapEntry g_maps[kMapCache];
+uint64_t g_stamp = 0;
+std::mutex g_map_mu;
+}  // namespace
+
+int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, int64_t rows,
+             int64_t ld_elems, int box_cols, int box_rows) {
+  const MapKey key{base, dtype, cols, rows, ld_elems, box_cols, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    for (auto& e : g_maps)
+      if (e.used && e.key == key) {
+        e.stamp = ++g_stamp;
+        *m = e.map;
+        return TIDE_OK;
+      }
+  }
   EncodeTiledFn enc = encode_fn();
   if (!enc) return set_error(TIDE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -517,6 +599,16 @@ static int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, i
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(TIDE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  MapEntry* victim = &g_maps[0];
+  for (auto& e : g_maps) {
+    if (!e.used) { victim = &e; break; }
+    if (e.stamp < victim->stamp) victim = &e;
+  }
+  victim->key = key;
+  victim->map = *m;
+  victim->stamp = ++g_stamp;
+  victim->used = true;
   return TIDE_OK;
 }
 
@@ -580,14 +672,20 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.ws = reinterpret_cast<Workspace*>(a.workspace);
   p.dbg = g_dbg;
   {
+    static const char* pf = getenv("TIDE_PREFETCH");
+    p.prefetch = pf ? atoi(pf) : 0;  // L2 prefetch measured slower: off by default
+  }
+  {
     static const char* env = getenv("TIDE_DEBUG_FLAGS");
     p.dbg_flags = env ? (uint32_t)atoi(env) : 0u;
   }
 
-  CUtensorMap tm_h128, tm_h32, tm_w, tm_g4;
+  CUtensorMap tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4;
   const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
   int rc;
   if ((rc = make_map(&tm_h128, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
+  if ((rc = make_map(&tm_h64, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 64))) return rc;
+  if ((rc = make_map(&tm_h32b, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 32))) return rc;
   if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, kGran))) return rc;
   if ((rc = make_map(&tm_g4, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 1))) return rc;
   if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
@@ -608,9 +706,9 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
     attr_set[dev & 63] = true;
   }
   if (a.dtype == TIDE_BF16)
-    route_tc_kernel<true><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h32, tm_w, tm_g4, p);
+    route_tc_kernel<true><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
   else
-    route_tc_kernel<false><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h32, tm_w, tm_g4, p);
+    route_tc_kernel<false><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
   return check_launch("route_tc_kernel");
 }
 

@@ -16,7 +16,7 @@ lib.tide_debug_timeline.argtypes = [ctypes.c_void_p]
 dbg = torch.zeros(148 * 24, dtype=torch.int64, device="cuda")
 for it in range(4):
     lib.tide_debug_timeline(dbg.data_ptr() if it == 3 else None)
-    P.route(h, router, theta=0.5, want_indices=True)
+    P.route(h, router, theta=0.5, want_indices=os.environ.get('TL_NOSCAN') != '1', want_mask=True)
 torch.cuda.synchronize()
 lib.tide_debug_timeline(None)
 t = dbg.view(148, 24).cpu().numpy().astype(np.int64)
@@ -31,6 +31,7 @@ for i, nm in enumerate(names):
 np.save("gpurun_out/timeline.npy", t)
 
 c = t[:, 16:22].astype(np.float64)
+c = c[(c[:, 1] > 0)]
 print("MMA thread: wait %.0f%% of %.0f cyc | producer: wait %.0f%% of %.0f cyc | rms warp: wait %.0f%% of %.0f cyc" % (
     100 * np.median(c[:, 0] / c[:, 1]), np.median(c[:, 1]), 100 * np.median(c[:, 2] / c[:, 3]), np.median(c[:, 3]),
     100 * np.median(c[:, 4] / c[:, 5]), np.median(c[:, 5])))

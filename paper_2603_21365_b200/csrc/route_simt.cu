@@ -5,11 +5,6 @@
 //   own dtype, where 1e-5 logit parity needs f32 products; b > 256; d % 8).
 //   16 rows x 128 bottleneck columns per pass, K staged through smem in
 //   chunks of 32, 2x4 register micro-tile per thread, f32 accumulation.
-// route_decode_kernel — the decode step (n <= 16 rows) for EVERY checkpoint
-//   in one launch: grid (checkpoint, K-split); partial pre-activations are
-//   reduced in a fixed order by the last CTA of each checkpoint (deterministic),
-//   and the last checkpoint to finish resolves the exit per row
-//   (ee/runtime.py:151-178).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -231,186 +226,4 @@ int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
   return check_launch("route_simt_kernel");
 }
 
-// ---------------------------------------------------------------------------
-// decode: all checkpoints, n <= 16 rows, one launch
-// ---------------------------------------------------------------------------
-constexpr int kMaxDecodeC = kMaxTickets;
-struct DecodeParams {
-  const void* h[kMaxDecodeC];
-  const void* w[kMaxDecodeC];
-  const float* wup[kMaxDecodeC];
-  int64_t layers[kMaxDecodeC];
-  int32_t C, d, b, ks;
-  int64_t ld_h, n, k_min;
-  int32_t mode;
-  float eps, inv_d, theta;
-  float* scores;
-  float* logits;
-  int64_t* exit_layers;
-  int64_t* exit_count;
-  Workspace* ws;
-};
-
-template <typename XT>
-__global__ void __launch_bounds__(kSThreads) route_decode_kernel(const DecodeParams p) {
-  __shared__ float Xs[kSR][kSK + 1];
-  __shared__ float Ws[kSJ][kSK + 1];
-  __shared__ float ss_s[kSR];
-  __shared__ const XT* xrow[kSR];
-  __shared__ unsigned int last_s;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int c = blockIdx.x, ks = blockIdx.y;
-  const int bstride = p.b;                       // floats per row of partial a
-  const int per_ks = kSR * bstride + kSR;        // partial a + partial sumsq
-  float* part = p.ws->partials + ((int64_t)c * p.ks + ks) * per_ks;
-  const int64_t kchunk = ((p.d + p.ks - 1) / p.ks + kSK - 1) / kSK * kSK;
-  const int64_t k0 = std::min<int64_t>((int64_t)ks * kchunk, p.d);
-  const int64_t k1 = std::min<int64_t>(k0 + kchunk, p.d);
-  const XT* h = reinterpret_cast<const XT*>(p.h[c]);
-  const XT* W = reinterpret_cast<const XT*>(p.w[c]);
-  if (tid < kSR) {
-    xrow[tid] = tid < p.n ? h + tid * p.ld_h : nullptr;
-    ss_s[tid] = 0.f;
-  }
-  __syncthreads();
-  for (int j0 = 0; j0 < p.b; j0 += kSJ) {
-    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    gemm_16x128<XT>(xrow, W, p.d, j0, p.b, k0, k1, acc, Xs, Ws, ss_s);
-#pragma unroll
-    for (int r2 = 0; r2 < 2; ++r2)
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int j = j0 + tx + 32 * cc;
-        if (j < p.b) part[(ty + 8 * r2) * bstride + j] = acc[r2][cc];
-      }
-  }
-  __syncthreads();
-  if (tid < kSR) part[kSR * bstride + tid] = ss_s[tid];
-  // ticket: the last K-split CTA of checkpoint c reduces in fixed order
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const unsigned int prev = atomicAdd(&p.ws->tickets[c], 1u);
-    last_s = (prev == (unsigned int)(p.ks - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (last_s) {
-    __threadfence();
-    float* base = p.ws->partials + (int64_t)c * p.ks * per_ks;
-    if (tid < kSR) {
-      float s = 0.f;
-      for (int q = 0; q < p.ks; ++q) s += base[(int64_t)q * per_ks + kSR * bstride + tid];
-      ss_s[tid] = s;
-    }
-    __syncthreads();
-    // warp ty owns rows ty, ty+8; lanes stride the bottleneck
-    for (int r2 = 0; r2 < 2; ++r2) {
-      const int r = ty + 8 * r2;
-      const float scale = rms_scale(ss_s[r], p.inv_d, p.eps);
-      float t = 0.f;
-      for (int j = tx; j < p.b; j += 32) {
-        float a = 0.f;
-        for (int q = 0; q < p.ks; ++q) a += base[(int64_t)q * per_ks + r * bstride + j];
-        t = fmaf(p.wup[c][j], silu_f32(__fmul_rn(a, scale)), t);
-      }
-      t = warp_sum_f32(t);
-      if (tx == 0 && r < p.n) {
-        if (p.scores) p.scores[(int64_t)c * p.n + r] = score_from_logit(t);
-        if (p.logits) p.logits[(int64_t)c * p.n + r] = t;
-        p.ws->dec_scores[c * kSR + r] = score_from_logit(t);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      p.ws->tickets[c] = 0;  // reset this checkpoint's ticket for the next launch
-      __threadfence();
-      const unsigned int prev = atomicAdd(&p.ws->ticket, 1u);
-      last_s = (prev == (unsigned int)(p.C - 1)) ? 2u : 0u;
-    }
-    __syncthreads();
-    if (last_s == 2u) {
-      __threadfence();
-      // exit resolution, rows in lanes of warp 0
-      if (ty == 0) {
-        const int r = tx;
-        int64_t exit_layer = TIDE_NO_EXIT;
-        if (p.mode == TIDE_MODE_PER_TOKEN) {
-          for (int cc = 0; cc < p.C && r < p.n; ++cc) {
-            if (p.layers[cc] < p.k_min) continue;
-            const float s = p.ws->dec_scores[cc * kSR + r];
-            if (s > p.theta) { exit_layer = p.layers[cc]; break; }
-          }
-        } else {
-          for (int cc = 0; cc < p.C; ++cc) {
-            if (p.layers[cc] < p.k_min) continue;
-            const bool fire =
-                r >= p.n || p.ws->dec_scores[cc * kSR + r] > p.theta;
-            if (__all_sync(0xffffffffu, fire)) { exit_layer = p.layers[cc]; break; }
-          }
-        }
-        if (r < p.n && p.exit_layers) p.exit_layers[r] = exit_layer;
-        const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, r < p.n && exit_layer != TIDE_NO_EXIT));
-        if (tx == 0) {
-          if (p.exit_count) p.exit_count[0] = cnt;
-          p.ws->ticket = 0;
-        }
-      }
-    }
-  }
-}
-
-int route_decode_launch(const DecodeParams& p0, int dtype, cudaStream_t stream) {
-  DecodeParams p = p0;
-  const int64_t per_ks = (int64_t)kSR * p.b + kSR;
-  int ks = std::max(1, std::min<int>((p.d + 255) / 256, 148 / std::max(1, p.C)));
-  while (ks > 1 && (int64_t)p.C * ks * per_ks > kMaxPartials) --ks;
-  if ((int64_t)p.C * ks * per_ks > kMaxPartials)
-    return set_error(TIDE_ERR_UNSUPPORTED, "decode problem too large for workspace");
-  p.ks = ks;
-  dim3 grid(p.C, ks);
-  switch (dtype) {
-    case TIDE_F32: route_decode_kernel<float><<<grid, kSThreads, 0, stream>>>(p); break;
-    case TIDE_BF16: route_decode_kernel<__nv_bfloat16><<<grid, kSThreads, 0, stream>>>(p); break;
-    case TIDE_F16: route_decode_kernel<__half><<<grid, kSThreads, 0, stream>>>(p); break;
-    default: return set_error(TIDE_ERR_ARG, "bad dtype %d", dtype);
-  }
-  return check_launch("route_decode_kernel");
-}
-
 }  // namespace tide
-
-extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n,
-                                 int32_t d, int32_t dtype, const void* const* w_ptrs,
-                                 const float* const* wup_ptrs, int32_t b, const int64_t* layers,
-                                 float eps, float theta, int64_t k_min, int32_t mode,
-                                 float* scores, float* logits, int64_t* exit_layers,
-                                 int64_t* exit_count, void* workspace, void* stream) {
-  using namespace tide;
-  if (C < 1 || C > kMaxDecodeC) return set_error(TIDE_ERR_ARG, "C must be in [1, %d]", kMaxDecodeC);
-  if (n < 1 || n > kSR) return set_error(TIDE_ERR_ARG, "decode rows must be in [1, %d]", kSR);
-  if (d < 1 || b < 1) return set_error(TIDE_ERR_ARG, "bad shape");
-  if (!workspace) return set_error(TIDE_ERR_ARG, "workspace required");
-  DecodeParams p{};
-  for (int c = 0; c < C; ++c) {
-    p.h[c] = h_ptrs[c];
-    p.w[c] = w_ptrs[c];
-    p.wup[c] = wup_ptrs[c];
-    p.layers[c] = layers[c];
-  }
-  p.C = C;
-  p.d = d;
-  p.b = b;
-  p.ld_h = ld_h;
-  p.n = n;
-  p.k_min = k_min;
-  p.mode = mode;
-  p.eps = eps;
-  p.inv_d = (float)(1.0 / (double)d);
-  p.theta = theta;
-  p.scores = scores;
-  p.logits = logits;
-  p.exit_layers = exit_layers;
-  p.exit_count = exit_count;
-  p.ws = reinterpret_cast<Workspace*>(workspace);
-  return route_decode_launch(p, dtype, reinterpret_cast<cudaStream_t>(stream));
-}

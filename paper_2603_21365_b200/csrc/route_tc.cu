@@ -289,6 +289,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         } else {
           // per tile: its slot is released as soon as ITS 4 MMAs retire
+          const uint32_t idesc = (p.dbg_flags & 128u) ? f16_idesc(kBF16 ? 1 : 0, 128, 64) : p.idesc;
+          const int ksteps = (p.dbg_flags & 256u) ? 2 : 4;
           for (int t = 0; t < T; ++t) {
             const long long w1 = clock64();
             mbar_wait(&a_full[as], aph);
@@ -298,10 +300,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               const uint64_t adesc =
                   desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * kASlotBytes) & 0x3FFFFu) >> 4);
               const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
+              for (int k = 0; k < ksteps; ++k)
                 if (!(p.dbg_flags & 2u))
-                  tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+                  tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, idesc, (kc | k) != 0);
               tc_commit(&a_empty[as]);
               if (kc == p.nk - 1) tc_commit(&t_full[t]);
             }
@@ -625,7 +626,11 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   while (cols < tpg * bp) cols <<= 1;
   const int nk = (a.d + 63) / 64;
   const uint32_t wslot = (uint32_t)npad * 128u;
-  const int nw = npad <= 128 ? 4 : 3;
+  int nw = npad <= 128 ? 4 : 3;
+  {
+    static const char* env = getenv("TIDE_NW");
+    if (env) nw = std::max(2, std::min(kMaxNW, atoi(env)));
+  }
   // smem carve-up (offsets from a 1024-aligned base)
   const uint32_t off_a = (uint32_t)nw * wslot;
   const int smem_cap = 227 * 1024;

@@ -182,7 +182,9 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
     eps = float(np.float32(bank.eps))
     code = D.dtype_code(final)
     b = bank.bottleneck if hasattr(bank, "bottleneck") else bank.routers[ckpts[0]].bottleneck
-    if n <= N.MAX_DECODE_ROWS:
+    vec = 4 if code == N.F32 else 8
+    decode_ok = d % vec == 0 and all(staged[k + 1].data_ptr() % 16 == 0 for k in ckpts)
+    if n <= N.MAX_DECODE_ROWS and decode_ok:
         ws_w = [device_weights(bank.routers[k], code, dev) for k in ckpts]
         mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
         cnt = torch.empty(1, dtype=torch.int64, device=dev)

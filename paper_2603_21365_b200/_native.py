@@ -63,6 +63,20 @@ _lib = None
 _lock = threading.Lock()
 
 
+def _check_fresh() -> None:
+    """The library must match the sources next to it (a stale .so would run
+    old kernels against new host code)."""
+    from . import build as _build
+    stamp = os.path.join(os.path.dirname(LIBPATH), "build.stamp")
+    if not os.path.exists(stamp):
+        return
+    with open(stamp) as fh:
+        if fh.read().strip() != _build._fingerprint():
+            raise NativeUnavailable(
+                f"{LIBPATH} is stale (sources changed since it was built); run "
+                "`python -m paper_2603_21365_b200.build`")
+
+
 def load(path: str = LIBPATH):
     """Load (once) and return the ctypes library with typed signatures."""
     global _lib
@@ -72,6 +86,8 @@ def load(path: str = LIBPATH):
                 raise NativeUnavailable(
                     f"{path} not built; run `python -m paper_2603_21365_b200.build` "
                     "(there is no CPU fallback)")
+            if path == LIBPATH and os.environ.get("TIDE_ALLOW_STALE") != "1":
+                _check_fresh()
             lib = ctypes.CDLL(path)
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(lib, name)

@@ -47,7 +47,8 @@ def _fingerprint() -> str:
             with open(os.path.join(d, f), "rb") as fh:
                 h.update(f.encode())
                 h.update(fh.read())
-    h.update(" ".join(ARCH + NVFLAGS).encode())
+    # flags without the absolute include path (the tree is relocated on GPU boxes)
+    h.update(" ".join(ARCH + [f for f in NVFLAGS if not f.startswith("-I")]).encode())
     return h.hexdigest()
 
 

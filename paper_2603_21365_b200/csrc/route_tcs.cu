@@ -1,0 +1,594 @@
+// K1s: split-K variant of K1 for small row counts (prefill shards of a few
+// thousand tokens, the later links of the peeling chain).
+//
+// Same contract and numerics as route_tc.cu (ee/router_ops.py:68-87 score,
+// ee/runtime.py:149,171 strict threshold, ee/router_ops.py:116-134 stable
+// compaction).  With n = 4,096 rows the persistent K1 gives each of 148 SMs
+// ~28 rows, so every SM re-reads all of W_down (1 MB at d = 4096) from L2 for
+// 56 KB of activations: the launch is bound by W re-reads and their latency,
+// not by HBM.  Here a 128-row tile is split over a cluster of KS CTAs along
+// d: CTA `rank` streams h[tile, K_rank] and W[:, K_rank] once (W traffic =
+// activation traffic), accumulates its partial D = h W^T in TMEM, and the
+// cluster reduces the partials through distributed shared memory:
+//   1. every CTA pushes column block c of its partial into the smem of the
+//      CTA that owns c (remote st.shared::cluster, no round trips), plus its
+//      partial sum of squares of each row to every CTA;
+//   2. cluster barrier; each CTA sums its columns over the KS partials in
+//      fixed rank order, applies scale / SiLU / w_up for them and pushes the
+//      partial logit of every row to rank 0;
+//   3. cluster barrier; rank 0 sums the KS partial logits (fixed order),
+//      thresholds, and compacts the tile with the same ordered look-back as
+//      K1 (partition = tile).
+// Deterministic (fixed reduction orders); not bit-identical to K1 (different
+// f32 summation order), both within the bf16 tolerance of the oracle.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tide {
+
+namespace {
+
+constexpr int kThreadsS = 192;  // producer, MMA issuer, 4 RMS / epilogue warps
+constexpr int kMaxStages = 8;
+constexpr int kASlot = 128 * 128;  // 128 rows x 64 cols x 2 B
+
+struct SplitParams {
+  int64_t n_host;
+  const int64_t* n_dev;
+  int64_t rows_total;
+  int32_t d, b, bp, nk, ks, cw, stages;
+  uint32_t idesc, tmem_cols, wslot, stage_bytes;
+  uint32_t off_recv, off_plog, off_wup, off_bar, off_words, off_tmem;
+  const int64_t* row_idx;
+  int32_t ids_from_rows;
+  const uint8_t* h_base;  // gathered rows are copied by the RMS warps (cp.async)
+  int64_t ld_bytes;
+  const float* w_up;
+  float eps, inv_d, theta;
+  int64_t layer;
+  float* scores;
+  float* logits;
+  uint8_t* mask;
+  int64_t* exit_idx;
+  int64_t* cont_idx;
+  int64_t* exit_layers;
+  int64_t* counts;
+  Workspace* ws;
+  unsigned long long* dbg;  // optional per-CTA timeline (globaltimer ns), 24 slots per CTA
+};
+
+__device__ __forceinline__ unsigned long long gtimer_s() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL(slot)                                                              \
+  do {                                                                        \
+    if (p.dbg) p.dbg[24 * blockIdx.x + (slot)] = gtimer_s();                  \
+  } while (0)
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cta address -> the same offset in CTA `rank`'s shared memory
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_dsmem_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+// bulk copy local smem -> smem of a CTA in the cluster, completing on its mbarrier
+__device__ __forceinline__ void bulk_s2dsmem(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                             uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(src_cta), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// split arrive / wait: every CTA of the cluster has started (its shared
+// memory may be written remotely) once the wait returns
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait;" ::: "memory"); }
+// 16-byte async copy global -> shared (zero-fills when src_bytes == 0) and the
+// mbarrier arrive that fires when this thread's prior cp.async have landed
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <bool kBF16>
+__global__ void __launch_bounds__(kThreadsS, 1)
+    route_tcs_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_w,
+                     const __grid_constant__ SplitParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // partials of this CTA's rows from the ks ranks: [src][bp][R], then ss [src][R]
+  float* recv = reinterpret_cast<float*>(smem + p.off_recv);
+  // after the stream both live in the (drained) stage ring: this CTA's staged
+  // partials [ks][bp][R] + ss [128], then the received ones
+  float* stage_out = reinterpret_cast<float*>(smem);
+  float* plog = reinterpret_cast<float*>(smem + p.off_plog);  // [column slice][R]
+  float* sWup = reinterpret_cast<float*>(smem + p.off_wup);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* acc_full = bars + 2 * kMaxStages;
+  uint64_t* recv_full = acc_full + 1;
+  uint32_t* words = reinterpret_cast<uint32_t*>(smem + p.off_words);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.off_tmem);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TL(0);
+  const uint32_t rank = cluster_rank();
+  const int64_t tile = blockIdx.x / p.ks;
+  const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
+  const int64_t ntiles = (n + 127) / 128;
+  const uint32_t tag = launch_tag(p.ws);
+  if (tile >= ntiles) {  // uniform over the cluster: no cluster barrier is pending
+    if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0 && p.counts) {
+      p.counts[0] = 0;
+      p.counts[1] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) launch_done(p.ws);
+    return;
+  }
+  const int64_t r0 = tile * 128;
+  const int64_t r1 = (r0 + 128 < n) ? r0 + 128 : n;
+  const int k0 = (int)((int64_t)p.nk * rank / p.ks), k1 = (int)((int64_t)p.nk * (rank + 1) / p.ks);
+  const bool gathered = p.row_idx != nullptr;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_w);
+    if (!gathered) prefetch_tmap(&tm_h);
+    for (int i = 0; i < p.stages; ++i) {
+      // gathered: + one cp.async arrive per RMS thread (they copy the rows)
+      mbar_init(&full[i], gathered ? 1 + 128 : 1);
+      mbar_init(&empty[i], 1 + 4);  // MMA commit + the 4 RMS warps
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(recv_full, 1);
+    // ks - 1 bulk copies of [bp + 1][128 / ks] floats land here (complete_tx may
+    // precede this expect_tx: the phase needs the arrive as well)
+    mbar_arrive_expect_tx(recv_full, (uint32_t)(p.ks - 1) * (uint32_t)(p.bp + 1) * (512u / p.ks));
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, p.tmem_cols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TL(1);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- producer
+    if (lane == 0) {
+      const uint64_t pol_h = policy_evict_first();
+      const uint64_t pol_w = policy_evict_last();
+      const uint32_t a_bytes = gathered ? 0u : (uint32_t)kASlot;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kc = k0; kc < k1; ++kc) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* sa = smem + (size_t)s * p.stage_bytes;
+        uint8_t* sw = sa + kASlot;
+        mbar_arrive_expect_tx(&full[s], a_bytes + p.wslot);
+        if (!gathered) tma_load_2d(sa, &tm_h, &full[s], kc * 64, (int)r0, pol_h);
+        tma_load_2d(sw, &tm_w, &full[s], kc * 64, 0, pol_w);
+        if (++s == p.stages) { s = 0; ph ^= 1u; }
+      }
+      TL(2);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    const uint64_t desc_hi = sw128_kmajor_desc(0);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kc = k0; kc < k1; ++kc) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      if (gathered) fence_proxy_async_smem();  // cp.async (generic proxy) -> MMA (async proxy)
+      if (elect_one()) {
+        const uint8_t* sa = smem + (size_t)s * p.stage_bytes;
+        const uint64_t adesc = desc_hi | (uint64_t)((smem_u32(sa) & 0x3FFFFu) >> 4);
+        const uint64_t bdesc = desc_hi | (uint64_t)((smem_u32(sa + kASlot) & 0x3FFFFu) >> 4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma_f16(tmem_base, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc != k0 || k != 0) ? 1u : 0u);
+        tc_commit(&empty[s]);
+        if (kc == k1 - 1) tc_commit(acc_full);
+      }
+      __syncwarp();
+      if (++s == p.stages) { s = 0; ph ^= 1u; }
+    }
+  } else {
+    // ------------------------------------------------------------- RMS partials
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const int row = 32 * q + lane;
+    const uint32_t swz = (uint32_t)(row & 7);
+    f32x2 ss0 = 0ull, ss1 = 0ull;
+    const int nkr = k1 - k0;
+    // Gathered rows (TMA gather4 measured ~2.5x slower than this): cp.async,
+    // `stages` chunks ahead.  The warp copies its own 32 rows; one instruction moves 4
+    // rows x 128 B (8 lanes per row, 16 B each) so every L2 request is whole
+    // sectors.  Offsets of this lane's 8 rows (rows 32q + 4it + lane/8) are
+    // kept in registers (-1 = past the end: left unwritten, never used).
+    const int sub = lane & 7, rg = lane >> 3;
+    int64_t src_off[8];
+    if (gathered) {
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int64_t r = r0 + 32 * q + 4 * it + rg;
+        src_off[it] = r < r1 ? p.row_idx[r] * p.ld_bytes : -1;
+      }
+    }
+    auto issue = [&](int i) {
+      const int si = i % p.stages;
+      mbar_wait(&empty[si], (((uint32_t)(i / p.stages)) & 1u) ^ 1u);
+      {
+        uint8_t* dst = smem + (size_t)si * p.stage_bytes;
+        const int64_t c = (int64_t)(k0 + i) * 64 + 8 * sub;  // this lane's 8 columns
+        const bool in = c < p.d;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rw = 32 * q + 4 * it + rg;
+          if (src_off[it] >= 0)
+            cp_async16(dst + rw * 128 + ((sub ^ (rw & 7)) << 4),
+                       p.h_base + src_off[it] + (in ? c * 2 : 0), in ? 16u : 0u);
+        }
+      }
+      cp_async_arrive_noinc(&full[si]);
+    };
+    if (gathered)
+      for (int i = 0; i < p.stages && i < nkr; ++i) issue(i);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kc = k0; kc < k1; ++kc) {
+      mbar_wait(&full[s], ph);
+      const uint8_t* rp = smem + (size_t)s * p.stage_bytes + row * 128;
+      uint4 u[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // refill the previous chunk's slot (its MMA has had a whole chunk to retire)
+      const int i = kc - k0;
+      if (gathered && i >= 1 && i - 1 + p.stages < nkr) issue(i - 1 + p.stages);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          f32x2 x;
+          if (kBF16) {
+            x = pack2u(w[e] << 16, w[e] & 0xFFFF0000u);
+          } else {
+            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+            x = pack2(f2.x, f2.y);
+          }
+          if (e & 1) ss1 = ffma2(x, x, ss1);
+          else ss0 = ffma2(x, x, ss0);
+        }
+      }
+      if (++s == p.stages) { s = 0; ph ^= 1u; }
+    }
+    float a0, a1, b0, b1;
+    unpack2(ss0, a0, a1);
+    unpack2(ss1, b0, b1);
+    const float ssp = (a0 + b0) + (a1 + b1);
+    for (int i = threadIdx.x - 64; i < p.b; i += 128) sWup[i] = p.w_up[i];  // used after recv_full
+    if (warp == 2 && lane == 0) TL(3);
+    mbar_wait(acc_full, 0);  // every MMA retired: the stage ring is no longer read by the MMAs
+    tc_fence_after();
+    epi_bar();               // ... nor by the other RMS warps
+    // the ring is drained: peers may copy their partials into it (recv) once
+    // every CTA of the cluster got here (this also proves they all started)
+    cluster_arrive_relaxed();
+    if (warp == 2 && lane == 0) TL(4);
+    // Stage this CTA's partials by destination: rank j owns rows [j R, (j+1) R)
+    // and gets them as one contiguous [bp][R] block (+ their R partial ss).
+    const int R = 128 / p.ks;
+    const int jo = row / R, rr = row - jo * R;
+    float* so = stage_out + (size_t)jo * p.bp * R + rr;
+    const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16);
+    for (int c0 = 0; c0 < p.bp; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(taddr + (uint32_t)c0, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) so[(size_t)(c0 + jj) * R] = __uint_as_float(v[jj]);
+    }
+    float* stage_ss = stage_out + (size_t)p.bp * 128;
+    stage_ss[row] = ssp;
+    tc_fence_before();
+    fence_proxy_async_smem();  // staged partials -> the bulk-copy (async) proxy
+    epi_bar();
+    cluster_wait();  // every ring in the cluster is drained
+    if (warp == 2 && lane == 0) {
+      const uint32_t blk = (uint32_t)p.bp * (uint32_t)R * 4u;
+      for (uint32_t j = 0; j < (uint32_t)p.ks; ++j) {
+        if (j == rank) continue;  // own rows are read from stage_out in place
+        const uint32_t bar = dsmem_addr(smem_u32(recv_full), j);
+        bulk_s2dsmem(dsmem_addr(smem_u32(recv) + rank * blk, j), smem_u32(stage_out) + j * blk, blk, bar);
+        bulk_s2dsmem(dsmem_addr(smem_u32(recv) + (uint32_t)p.ks * blk + rank * (uint32_t)R * 4u, j),
+                     smem_u32(stage_ss + j * R), (uint32_t)R * 4u, bar);
+      }
+      TL(5);
+    }
+  }
+  if (warp < 2) {
+    cluster_arrive_relaxed();  // (the epilogue warps arrive once the ring is drained ...
+    cluster_wait();
+    cluster_arrive_relaxed();  // ... and once the partials of their rows landed)
+  }
+
+  if (warp >= 2) {
+    mbar_wait(recv_full, 0);
+    // every copy INTO this CTA has landed; once all CTAs arrive, every copy
+    // FROM this CTA's smem has been read, so it may exit
+    cluster_arrive_relaxed();
+    if (threadIdx.x == 64) TL(6);
+    // This CTA's rows [rank R, (rank+1) R): thread t sums column slice t / R
+    // of row t % R over the ks partials (fixed order) and applies SiLU / w_up.
+    const int R = 128 / p.ks;
+    const int t = threadIdx.x - 64;
+    const int rr = t % R, sl = t / R;
+    // source j's [bp][R] block: received, or (j == rank) still in stage_out
+    const float* own = stage_out + (size_t)rank * p.bp * R + rr;
+    const float* rss = recv + (size_t)p.ks * p.bp * R + rr;
+    float ss = 0.f;
+    for (int j = 0; j < p.ks; ++j)
+      ss += (j == (int)rank) ? stage_out[(size_t)p.bp * 128 + rank * R + rr] : rss[j * R];
+    const float scale = rms_scale(ss, p.inv_d, p.eps);
+    const f32x2 scale2 = pack2(scale, scale);
+    const float nsl = -scale * 1.4426950408889634f;
+    const f32x2 nsl2 = pack2(nsl, nsl);
+    // 8 columns at a time: 8 independent sums, then 4 independent SiLU pairs
+    // (one warp per SMSP here, so ILP is what hides the latency)
+    f32x2 acc2 = 0ull, acc2b = 0ull;
+    const int cbase = sl * p.cw;
+    for (int cl0 = 0; cl0 < p.cw; cl0 += 8) {
+      if (cbase + cl0 >= p.b) break;
+      float sum[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum[u] = 0.f;
+      for (int j = 0; j < p.ks; ++j) {
+        const float* src = ((j == (int)rank) ? own : recv + (size_t)j * p.bp * R + rr) +
+                           (size_t)(cbase + cl0) * R;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum[u] += src[u * R];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        const int c = cbase + cl0 + u;
+        const float w0 = c < p.b ? sWup[c] : 0.f;
+        const float w1 = c + 1 < p.b ? sWup[c + 1] : 0.f;
+        const float a0 = c < p.b ? sum[u] : 0.f;
+        const float a1 = c + 1 < p.b ? sum[u + 1] : 0.f;
+        const f32x2 tt = ffma2(pack2(w0, w1), silu2_fast(pack2(a0, a1), scale2, nsl2), 0ull);
+        if (u & 2) acc2b = fadd2(acc2b, tt);
+        else acc2 = fadd2(acc2, tt);
+      }
+    }
+    acc2 = fadd2(acc2, acc2b);
+    float lo, hi;
+    unpack2(acc2, lo, hi);
+    plog[sl * R + rr] = lo + hi;
+    epi_bar();
+    // rows of this partition: threads t < R finish them (fixed slice order)
+    const int64_t pr0 = r0 + (int64_t)rank * R;
+    const int64_t pr1 = (pr0 + R < r1) ? pr0 + R : (pr0 < r1 ? r1 : pr0);
+    bool ex = false;
+    if (t < R) {
+      float logit = 0.f;
+      for (int j = 0; j < p.ks; ++j) logit += plog[j * R + t];
+      const int64_t r = pr0 + t;
+      if (r < pr1) {
+        const float score = score_from_logit(logit);
+        ex = score > p.theta;
+        if (p.scores) p.scores[r] = score;
+        if (p.logits) p.logits[r] = logit;
+        if (p.mask) p.mask[r] = ex ? 1 : 0;
+        if (ex && p.exit_layers) p.exit_layers[gathered ? p.row_idx[r] : r] = p.layer;
+      }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, ex);
+    if (lane == 0 && t < R) words[t >> 5] = bal;
+    epi_bar();
+    if (warp == 2 && (p.exit_idx || p.cont_idx || p.counts)) {
+      const int nw = (R + 31) / 32;
+      const uint32_t word = lane < nw ? words[lane] : 0u;
+      const uint32_t cnt = __popc(word);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl_w = incl - cnt;
+      const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+      const int64_t part = tile * p.ks + rank;
+      const uint32_t E = lookback_exclusive(p.ws->status, tag, part, agg);
+      if (lane == 0) TL(8);
+      if (p.exit_idx || p.cont_idx) {
+        const uint32_t lt = (1u << lane) - 1u;
+        for (int w = 0; w < nw; ++w) {
+          const uint32_t wd = __shfl_sync(0xffffffffu, word, w);
+          const uint32_t pre = __shfl_sync(0xffffffffu, excl_w, w);
+          const int64_t r = pr0 + 32 * w + lane;
+          if (r < pr1) {
+            const int64_t rank_e = (int64_t)E + pre + __popc(wd & lt);
+            const int64_t id = (p.ids_from_rows && gathered) ? p.row_idx[r] : r;
+            if ((wd >> lane) & 1u) {
+              if (p.exit_idx) p.exit_idx[rank_e] = id;
+            } else if (p.cont_idx) {
+              p.cont_idx[r - rank_e] = id;
+            }
+          }
+        }
+      }
+      if (part == ntiles * p.ks - 1 && lane == 0 && p.counts) {
+        p.counts[0] = (int64_t)E + agg;
+        p.counts[1] = n - ((int64_t)E + agg);
+      }
+    }
+  }
+  if (threadIdx.x == 64) TL(7);
+  cluster_wait();  // every bulk copy out of this CTA's smem has been read
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+  if (threadIdx.x == 0) {
+    TL(9);
+    launch_done(p.ws);
+  }
+}
+
+}  // namespace
+
+// Split factor for this launch, 0 = use the persistent K1.  KS in {2, 4, 8}
+// (power of two; column blocks of bp / KS, a multiple of 16), tiles x KS <= SM count, and at
+// least one 64-column k-chunk per rank.
+int route_tcs_split(int64_t n, int d, int b, int sms) {
+  // TIDE_SPLIT: "0" forces the persistent K1, 2/4/8 caps the split (tests, sweeps)
+  const char* env = getenv("TIDE_SPLIT");
+  const int cap = env ? atoi(env) : 8;
+  if (cap <= 1) return 0;
+  const int npad = (b + 15) / 16 * 16;
+  if (npad > 128 || n < 1) return 0;
+  const int64_t tiles = (n + 127) / 128;
+  const int nk = (d + 63) / 64;
+  const int bp = (npad + 31) / 32 * 32;
+  int ks = 8;
+  while (ks > 1 && (ks > cap || tiles * ks > sms || ks > nk || bp % (16 * ks) != 0)) ks >>= 1;
+  return ks >= 2 ? ks : 0;
+}
+
+int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks) {
+  SplitParams p{};
+  const int npad = (a.b + 15) / 16 * 16;
+  const int bp = (npad + 31) / 32 * 32;
+  p.n_host = a.n;
+  p.n_dev = a.n_dev;
+  p.rows_total = a.rows_total;
+  p.d = a.d;
+  p.b = a.b;
+  p.bp = bp;
+  p.nk = (a.d + 63) / 64;
+  p.ks = ks;
+  p.cw = bp / ks;
+  p.idesc = f16_idesc(a.dtype == TIDE_BF16 ? 1 : 0, 128, npad);
+  p.tmem_cols = bp <= 32 ? 32 : bp <= 64 ? 64 : 128;
+  p.wslot = (uint32_t)npad * 128u;
+  p.stage_bytes = (uint32_t)kASlot + p.wslot;
+  // staged + received partials reuse the stage ring; small fixed regions after it
+  const uint32_t part_bytes = ((uint32_t)(bp + 1) * 512u + 1023u) & ~1023u;
+  const uint32_t fixed = 512u /*plog*/ + 1024u /*w_up*/ + 256u /*bars*/ + 64u /*words*/ + 16u;
+  const int smem_cap = 227 * 1024 - 1024;
+  const int stages = std::min<int>(kMaxStages, (int)((smem_cap - (int)fixed) / (int)p.stage_bytes));
+  if (stages < 2 || 2u * part_bytes > (uint32_t)stages * p.stage_bytes)
+    return set_error(TIDE_ERR_UNSUPPORTED, "split route: smem too small");
+  p.stages = stages;
+  p.off_recv = part_bytes;
+  p.off_plog = (uint32_t)stages * p.stage_bytes;
+  p.off_wup = p.off_plog + 512u;
+  p.off_bar = p.off_wup + 1024u;
+  p.off_words = p.off_bar + 256u;
+  p.off_tmem = p.off_words + 64u;
+  const uint32_t smem_bytes = p.off_tmem + 16u + 1024u;
+  p.row_idx = a.row_idx;
+  p.ids_from_rows = a.ids_from_rows;
+  p.h_base = reinterpret_cast<const uint8_t*>(a.h);
+  p.ld_bytes = a.ld_h * 2;
+  p.w_up = a.w_up;
+  p.eps = a.eps;
+  p.inv_d = (float)(1.0 / (double)a.d);
+  p.theta = a.theta;
+  p.layer = a.layer;
+  p.scores = a.scores;
+  p.logits = a.logits;
+  p.mask = a.mask;
+  p.exit_idx = a.exit_idx;
+  p.cont_idx = a.cont_idx;
+  p.exit_layers = a.exit_layers;
+  p.counts = a.counts;
+  p.ws = reinterpret_cast<Workspace*>(a.workspace);
+  p.dbg = g_dbg;
+
+  const int64_t tiles = (a.n + 127) / 128;
+  if (tiles * ks > kMaxParts / 2) return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
+  CUtensorMap tm_h, tm_w;
+  const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
+  int rc;
+  if ((rc = make_map(&tm_h, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
+  if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
+
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[64] = {false};
+  if (!attr_set[dev & 63]) {
+    cudaFuncSetAttribute(route_tcs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(route_tcs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set[dev & 63] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(tiles * ks), 1, 1);
+  cfg.blockDim = dim3(kThreadsS, 1, 1);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)ks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (a.dtype == TIDE_BF16)
+    e = cudaLaunchKernelEx(&cfg, route_tcs_kernel<true>, tm_h, tm_w, p);
+  else
+    e = cudaLaunchKernelEx(&cfg, route_tcs_kernel<false>, tm_h, tm_w, p);
+  if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "route_tcs_kernel: %s", cudaGetErrorString(e));
+  return check_launch("route_tcs_kernel");
+}
+
+}  // namespace tide

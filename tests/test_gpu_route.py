@@ -98,8 +98,18 @@ def test_tensor_core_path_selected():
     assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 128) == 0
 
 
-@pytest.mark.parametrize("n", [1, 31, 32, 33, 127, 128, 129, 500, 4099, 20000])
-def test_ragged_sizes_bf16(n):
+@pytest.fixture(params=["split", "persistent"])
+def k1_mode(request, monkeypatch):
+    """Small row counts take the split-K cluster kernel unless TIDE_SPLIT=0."""
+    if request.param == "persistent":
+        monkeypatch.setenv("TIDE_SPLIT", "0")
+    else:
+        monkeypatch.delenv("TIDE_SPLIT", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 127, 128, 129, 500, 4099, 9500, 20000])
+def test_ragged_sizes_bf16(n, k1_mode):
     """Every tile / group boundary: 32-row boxes, partial tiles, multi-group CTAs."""
     need_gpu()
     g = np.random.Generator(np.random.PCG64(1000 + n))
@@ -117,7 +127,7 @@ def test_ragged_sizes_bf16(n):
     np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
 
 
-def test_gathered_rows_equal_dense_on_subset():
+def test_gathered_rows_equal_dense_on_subset(k1_mode):
     """row_idx (peeling) mode == dense route over h[row_idx]; ids mapped back."""
     need_gpu()
     g = np.random.Generator(np.random.PCG64(77))
@@ -154,7 +164,7 @@ def test_gathered_rows_equal_dense_on_subset():
     assert np.all(el[sub[mk]] == 9) and np.all(el[np.setdiff1d(np.arange(n), sub[mk])] == -1)
 
 
-def test_device_count_input():
+def test_device_count_input(k1_mode):
     """n read from device memory (the peeling chain's counts[1])."""
     need_gpu()
     g = np.random.Generator(np.random.PCG64(78))
@@ -196,3 +206,28 @@ def test_repeated_launches_reuse_workspace():
         e, c = O.compact_indices(r["mask"].cpu().numpy())
         np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
         np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("d,b,n", [(200, 40, 700), (1000, 96, 3000), (4096, 128, 4096),
+                                   (8192, 16, 1500), (8192, 128, 8192), (512, 256, 300)])
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_split_and_persistent_agree_with_oracle(d, b, n, dtype, monkeypatch):
+    """Both K1 variants (split-K cluster / persistent) against the oracle, incl.
+    widths that are not multiples of 64 and bottlenecks that are not of 32."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(d * 7 + b + n))
+    wd = (g.standard_normal((b, d)) * (1.0 / np.sqrt(d))).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = O.round_to(g.standard_normal((n, d), dtype=np.float32), dtype)
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TIDE_SPLIT", mode)
+        r = P.route(to_dev(h, dtype), _router(wd, wu), theta=0.5, want_logits=True,
+                    want_indices=True)
+        check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, dtype, f"split={mode}")
+        e, c = O.compact_indices(r["mask"].cpu().numpy())
+        np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+        np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+        out[mode] = r["logits"].cpu().numpy()
+    np.testing.assert_allclose(out["1"], out["0"], rtol=1e-4, atol=1e-5)

@@ -45,8 +45,8 @@ int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, int64_t 
 extern unsigned long long* g_dbg;
 int route_tc2_launch(const RouteArgs& a, cudaStream_t stream);
 int route_tc_launch(const RouteArgs& a, cudaStream_t stream);
-int route_tcs_split(int64_t n, int d, int b, int sms);
-int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks);
+int route_tcs_plan(const RouteArgs& a, int dev, int* grid);
+int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid);
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream);
 int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
                    int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,

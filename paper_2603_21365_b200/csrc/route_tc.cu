@@ -623,8 +623,9 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
     // few rows: split d over a cluster instead (route_tcs.cu)
     int dev0 = 0;
     cudaGetDevice(&dev0);
-    const int ks = route_tcs_split(a.n, a.d, a.b, sm_count(dev0));
-    if (ks) return route_tcs_launch(a, stream, ks);
+    int grid = 0;
+    const int ks = route_tcs_plan(a, dev0, &grid);
+    if (ks) return route_tcs_launch(a, stream, ks, grid);
   }
   const int npad = (a.b + 15) / 16 * 16;
   const int bp = (npad + 31) / 32 * 32;

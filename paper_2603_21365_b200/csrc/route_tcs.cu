@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -151,23 +152,36 @@ __global__ void __launch_bounds__(kThreadsS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TL(0);
-  const uint32_t rank = cluster_rank();
-  const int64_t tile = blockIdx.x / p.ks;
+  // The cluster (p.ks CTAs, the largest split the shape allows) is cut into
+  // groups of ks CTAs, one 128-row tile per group, ks chosen HERE from the live
+  // row count (n may come from device memory: later links of a peeling chain
+  // split their few remaining tiles further).
+  const uint32_t crank = cluster_rank();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
   const int64_t ntiles = (n + 127) / 128;
+  int ks = p.ks;
+  while (ks > 1 && ntiles * ks > (int64_t)gridDim.x) ks >>= 1;
+  const uint32_t rank = crank % (uint32_t)ks, gbase = crank - rank;
+  const int64_t tile = (int64_t)(blockIdx.x / p.ks) * (p.ks / ks) + crank / (uint32_t)ks;
+  const int cw = p.bp / ks;
   const uint32_t tag = launch_tag(p.ws);
-  if (tile >= ntiles) {  // uniform over the cluster: no cluster barrier is pending
+  if (tile >= ntiles) {
+    // idle (its whole group is): still takes part in the two cluster barriers
     if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0 && p.counts) {
       p.counts[0] = 0;
       p.counts[1] = 0;
     }
+    cluster_arrive_relaxed();
+    cluster_wait();
+    cluster_arrive_relaxed();
+    cluster_wait();
     __syncthreads();
     if (threadIdx.x == 0) launch_done(p.ws);
     return;
   }
   const int64_t r0 = tile * 128;
   const int64_t r1 = (r0 + 128 < n) ? r0 + 128 : n;
-  const int k0 = (int)((int64_t)p.nk * rank / p.ks), k1 = (int)((int64_t)p.nk * (rank + 1) / p.ks);
+  const int k0 = (int)((int64_t)p.nk * rank / ks), k1 = (int)((int64_t)p.nk * (rank + 1) / ks);
   const bool gathered = p.row_idx != nullptr;
 
   if (warp == 0 && lane == 0) {
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     mbar_init(recv_full, 1);
     // ks - 1 bulk copies of [bp + 1][128 / ks] floats land here (complete_tx may
     // precede this expect_tx: the phase needs the arrive as well)
-    mbar_arrive_expect_tx(recv_full, (uint32_t)(p.ks - 1) * (uint32_t)(p.bp + 1) * (512u / p.ks));
+    mbar_arrive_expect_tx(recv_full, (uint32_t)(ks - 1) * (uint32_t)(p.bp + 1) * (512u / ks));
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     if (warp == 2 && lane == 0) TL(4);
     // Stage this CTA's partials by destination: rank j owns rows [j R, (j+1) R)
     // and gets them as one contiguous [bp][R] block (+ their R partial ss).
-    const int R = 128 / p.ks;
+    const int R = 128 / ks;
     const int jo = row / R, rr = row - jo * R;
     float* so = stage_out + (size_t)jo * p.bp * R + rr;
     const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16);
@@ -342,11 +356,12 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     cluster_wait();  // every ring in the cluster is drained
     if (warp == 2 && lane == 0) {
       const uint32_t blk = (uint32_t)p.bp * (uint32_t)R * 4u;
-      for (uint32_t j = 0; j < (uint32_t)p.ks; ++j) {
+      for (uint32_t j = 0; j < (uint32_t)ks; ++j) {
         if (j == rank) continue;  // own rows are read from stage_out in place
-        const uint32_t bar = dsmem_addr(smem_u32(recv_full), j);
-        bulk_s2dsmem(dsmem_addr(smem_u32(recv) + rank * blk, j), smem_u32(stage_out) + j * blk, blk, bar);
-        bulk_s2dsmem(dsmem_addr(smem_u32(recv) + (uint32_t)p.ks * blk + rank * (uint32_t)R * 4u, j),
+        const uint32_t bar = dsmem_addr(smem_u32(recv_full), gbase + j);
+        bulk_s2dsmem(dsmem_addr(smem_u32(recv) + rank * blk, gbase + j), smem_u32(stage_out) + j * blk,
+                     blk, bar);
+        bulk_s2dsmem(dsmem_addr(smem_u32(recv) + (uint32_t)ks * blk + rank * (uint32_t)R * 4u, gbase + j),
                      smem_u32(stage_ss + j * R), (uint32_t)R * 4u, bar);
       }
       TL(5);
@@ -366,14 +381,14 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     if (threadIdx.x == 64) TL(6);
     // This CTA's rows [rank R, (rank+1) R): thread t sums column slice t / R
     // of row t % R over the ks partials (fixed order) and applies SiLU / w_up.
-    const int R = 128 / p.ks;
+    const int R = 128 / ks;
     const int t = threadIdx.x - 64;
     const int rr = t % R, sl = t / R;
     // source j's [bp][R] block: received, or (j == rank) still in stage_out
     const float* own = stage_out + (size_t)rank * p.bp * R + rr;
-    const float* rss = recv + (size_t)p.ks * p.bp * R + rr;
+    const float* rss = recv + (size_t)ks * p.bp * R + rr;
     float ss = 0.f;
-    for (int j = 0; j < p.ks; ++j)
+    for (int j = 0; j < ks; ++j)
       ss += (j == (int)rank) ? stage_out[(size_t)p.bp * 128 + rank * R + rr] : rss[j * R];
     const float scale = rms_scale(ss, p.inv_d, p.eps);
     const f32x2 scale2 = pack2(scale, scale);
@@ -382,13 +397,13 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     // 8 columns at a time: 8 independent sums, then 4 independent SiLU pairs
     // (one warp per SMSP here, so ILP is what hides the latency)
     f32x2 acc2 = 0ull, acc2b = 0ull;
-    const int cbase = sl * p.cw;
-    for (int cl0 = 0; cl0 < p.cw; cl0 += 8) {
+    const int cbase = sl * cw;
+    for (int cl0 = 0; cl0 < cw; cl0 += 8) {
       if (cbase + cl0 >= p.b) break;
       float sum[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) sum[u] = 0.f;
-      for (int j = 0; j < p.ks; ++j) {
+      for (int j = 0; j < ks; ++j) {
         const float* src = ((j == (int)rank) ? own : recv + (size_t)j * p.bp * R + rr) +
                            (size_t)(cbase + cl0) * R;
 #pragma unroll
@@ -417,7 +432,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     bool ex = false;
     if (t < R) {
       float logit = 0.f;
-      for (int j = 0; j < p.ks; ++j) logit += plog[j * R + t];
+      for (int j = 0; j < ks; ++j) logit += plog[j * R + t];
       const int64_t r = pr0 + t;
       if (r < pr1) {
         const float score = score_from_logit(logit);
@@ -443,7 +458,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       }
       const uint32_t excl_w = incl - cnt;
       const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
-      const int64_t part = tile * p.ks + rank;
+      const int64_t part = tile * ks + rank;
       const uint32_t E = lookback_exclusive(p.ws->status, tag, part, agg);
       if (lane == 0) TL(8);
       if (p.exit_idx || p.cont_idx) {
@@ -463,7 +478,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
           }
         }
       }
-      if (part == ntiles * p.ks - 1 && lane == 0 && p.counts) {
+      if (part == ntiles * ks - 1 && lane == 0 && p.counts) {
         p.counts[0] = (int64_t)E + agg;
         p.counts[1] = n - ((int64_t)E + agg);
       }
@@ -485,28 +500,116 @@ __global__ void __launch_bounds__(kThreadsS, 1)
 
 }  // namespace
 
-// Split factor for this launch, 0 = use the persistent K1.  KS in {2, 4, 8}
-// (power of two; column blocks of bp / KS, a multiple of 16), tiles x KS <= SM count, and at
-// least one 64-column k-chunk per rank.
-int route_tcs_split(int64_t n, int d, int b, int sms) {
+namespace {
+
+struct TcsLayout {
+  int npad, bp, stages;
+  uint32_t wslot, stage_bytes, off_recv, off_plog, off_wup, off_bar, off_words, off_tmem, smem_bytes;
+};
+
+// Shared-memory carve-up (depends on the bottleneck width only).  The staged
+// and received partials reuse the drained stage ring; small fixed regions after.
+bool tcs_layout(int b, TcsLayout& L) {
+  L.npad = (b + 15) / 16 * 16;
+  L.bp = (L.npad + 31) / 32 * 32;
+  L.wslot = (uint32_t)L.npad * 128u;
+  L.stage_bytes = (uint32_t)kASlot + L.wslot;
+  const uint32_t part_bytes = ((uint32_t)(L.bp + 1) * 512u + 1023u) & ~1023u;
+  const uint32_t fixed = 512u /*plog*/ + 1024u /*w_up*/ + 256u /*bars*/ + 64u /*words*/ + 16u;
+  const int smem_cap = 227 * 1024 - 1024;
+  L.stages = std::min<int>(kMaxStages, (int)((smem_cap - (int)fixed) / (int)L.stage_bytes));
+  if (L.npad > 128 || L.stages < 2 || 2u * part_bytes > (uint32_t)L.stages * L.stage_bytes) return false;
+  L.off_recv = part_bytes;
+  L.off_plog = (uint32_t)L.stages * L.stage_bytes;
+  L.off_wup = L.off_plog + 512u;
+  L.off_bar = L.off_wup + 1024u;
+  L.off_words = L.off_bar + 256u;
+  L.off_tmem = L.off_words + 64u;
+  L.smem_bytes = L.off_tmem + 16u + 1024u;
+  return true;
+}
+
+void tcs_set_attrs(int dev) {
+  static bool attr_set[64] = {false};
+  if (!attr_set[dev & 63]) {
+    cudaFuncSetAttribute(route_tcs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(route_tcs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set[dev & 63] = true;
+  }
+}
+
+// Co-resident clusters of size c (a cluster lives in one GPC, so this is less
+// than SMs / c: e.g. clusters of 8 leave several SMs of every GPC idle).
+int tcs_max_clusters(int dev, int c, uint32_t smem) {
+  static int cache[64][4][2];  // [dev][c = 2, 4, 8][smem class]
+  const int ci = c == 2 ? 0 : c == 4 ? 1 : 2;
+  const int si = smem > 200 * 1024 ? 1 : 0;
+  int& mc = cache[dev & 63][ci][si];
+  if (!mc) {
+    tcs_set_attrs(dev);
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3((unsigned)(c * 64), 1, 1);
+    q.blockDim = dim3(kThreadsS, 1, 1);
+    q.dynamicSmemBytes = smem;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = (unsigned)c;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int v = 0;
+    if (cudaOccupancyMaxActiveClusters(&v, route_tcs_kernel<true>, &q) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = sm_count(dev) / (2 * c);
+    }
+    mc = v;
+    if (getenv("TIDE_DEBUG_PLAN"))
+      fprintf(stderr, "[tide] clusters of %d x %u B smem: %d co-resident\n", c, smem, v);
+  }
+  return mc;
+}
+
+}  // namespace
+
+// Launch plan: cluster size C (the largest split, 0 = use the persistent K1)
+// and grid.  Dense launches (row count known on the host): the largest C whose
+// co-resident clusters give every tile a full cluster.  Chain links (row
+// count in device memory, usually far below the capacity `n`): the largest C
+// whose co-resident CTAs cover every tile of the capacity at split 1 — the
+// kernel picks the split from the live count (a link that still holds most
+// rows runs at split 1-2 on fewer SMs; the links after a large exit wave run
+// at split 8).  C in {2, 4, 8}: bp / C a multiple of 16 and
+// at least one 64-column k-chunk per rank.
+int route_tcs_plan(const RouteArgs& a, int dev, int* grid) {
   // TIDE_SPLIT: "0" forces the persistent K1, 2/4/8 caps the split (tests, sweeps)
   const char* env = getenv("TIDE_SPLIT");
   const int cap = env ? atoi(env) : 8;
-  if (cap <= 1) return 0;
-  const int npad = (b + 15) / 16 * 16;
-  if (npad > 128 || n < 1) return 0;
-  const int64_t tiles = (n + 127) / 128;
-  const int nk = (d + 63) / 64;
-  const int bp = (npad + 31) / 32 * 32;
-  int ks = 8;
-  while (ks > 1 && (ks > cap || tiles * ks > sms || ks > nk || bp % (16 * ks) != 0)) ks >>= 1;
-  return ks >= 2 ? ks : 0;
+  TcsLayout L;
+  if (cap <= 1 || a.n < 1 || !tcs_layout(a.b, L)) return 0;
+  const int64_t tiles = (a.n + 127) / 128;
+  const int nk = (a.d + 63) / 64;
+  const bool live = a.n_dev != nullptr;
+  for (int c = 8; c >= 2; c >>= 1) {
+    if (c > cap || c > nk || L.bp % (16 * c) != 0) continue;
+    const int64_t mc = tcs_max_clusters(dev, c, L.smem_bytes);
+    if (!live && tiles <= mc) {
+      *grid = (int)(tiles * c);
+      return c;
+    }
+    if (live && tiles <= mc * c) {
+      *grid = (int)(std::min<int64_t>(mc, tiles) * c);
+      return c;
+    }
+  }
+  return 0;
 }
 
-int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks) {
+int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) {
   SplitParams p{};
-  const int npad = (a.b + 15) / 16 * 16;
-  const int bp = (npad + 31) / 32 * 32;
+  TcsLayout L;
+  if (!tcs_layout(a.b, L)) return set_error(TIDE_ERR_UNSUPPORTED, "split route: smem too small");
+  const int npad = L.npad, bp = L.bp;
   p.n_host = a.n;
   p.n_dev = a.n_dev;
   p.rows_total = a.rows_total;
@@ -518,23 +621,16 @@ int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks) {
   p.cw = bp / ks;
   p.idesc = f16_idesc(a.dtype == TIDE_BF16 ? 1 : 0, 128, npad);
   p.tmem_cols = bp <= 32 ? 32 : bp <= 64 ? 64 : 128;
-  p.wslot = (uint32_t)npad * 128u;
-  p.stage_bytes = (uint32_t)kASlot + p.wslot;
-  // staged + received partials reuse the stage ring; small fixed regions after it
-  const uint32_t part_bytes = ((uint32_t)(bp + 1) * 512u + 1023u) & ~1023u;
-  const uint32_t fixed = 512u /*plog*/ + 1024u /*w_up*/ + 256u /*bars*/ + 64u /*words*/ + 16u;
-  const int smem_cap = 227 * 1024 - 1024;
-  const int stages = std::min<int>(kMaxStages, (int)((smem_cap - (int)fixed) / (int)p.stage_bytes));
-  if (stages < 2 || 2u * part_bytes > (uint32_t)stages * p.stage_bytes)
-    return set_error(TIDE_ERR_UNSUPPORTED, "split route: smem too small");
-  p.stages = stages;
-  p.off_recv = part_bytes;
-  p.off_plog = (uint32_t)stages * p.stage_bytes;
-  p.off_wup = p.off_plog + 512u;
-  p.off_bar = p.off_wup + 1024u;
-  p.off_words = p.off_bar + 256u;
-  p.off_tmem = p.off_words + 64u;
-  const uint32_t smem_bytes = p.off_tmem + 16u + 1024u;
+  p.wslot = L.wslot;
+  p.stage_bytes = L.stage_bytes;
+  p.stages = L.stages;
+  p.off_recv = L.off_recv;
+  p.off_plog = L.off_plog;
+  p.off_wup = L.off_wup;
+  p.off_bar = L.off_bar;
+  p.off_words = L.off_words;
+  p.off_tmem = L.off_tmem;
+  const uint32_t smem_bytes = L.smem_bytes;
   p.row_idx = a.row_idx;
   p.ids_from_rows = a.ids_from_rows;
   p.h_base = reinterpret_cast<const uint8_t*>(a.h);
@@ -564,14 +660,9 @@ int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks) {
 
   int dev = 0;
   cudaGetDevice(&dev);
-  static bool attr_set[64] = {false};
-  if (!attr_set[dev & 63]) {
-    cudaFuncSetAttribute(route_tcs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(route_tcs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set[dev & 63] = true;
-  }
+  tcs_set_attrs(dev);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(tiles * ks), 1, 1);
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
   cfg.blockDim = dim3(kThreadsS, 1, 1);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;

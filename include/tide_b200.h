@@ -45,7 +45,7 @@ extern "C" {
 #define TIDE_MODE_BATCH_UNANIMOUS 1 /* ee/runtime.py:29 */
 #define TIDE_NO_EXIT (-1)           /* ee/runtime.py:35 */
 
-#define TIDE_WORKSPACE_BYTES (4u << 20)
+#define TIDE_WORKSPACE_BYTES (8u << 20)
 #define TIDE_MAX_LAYERS 256
 #define TIDE_MAX_DECODE_ROWS 16
 

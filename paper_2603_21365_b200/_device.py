@@ -67,13 +67,17 @@ _ws_lock = threading.Lock()
 _workspaces: dict = {}
 
 
-def workspace(device=None) -> torch.Tensor:
-    """The look-back workspace of the current stream (allocated + zeroed once)."""
+def workspace(device=None, stream: int = None) -> torch.Tensor:
+    """The look-back workspace of the current stream (allocated + zeroed once).
+    `stream` (the raw handle, when the caller already has it) saves a lookup."""
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
-    s = stream_handle(dev)
+    s = stream_handle(dev) if stream is None else stream
     key = (dev.index, s)
+    ws = _workspaces.get(key)
+    if ws is not None:
+        return ws
     with _ws_lock:
         ws = _workspaces.get(key)
         if ws is None:

@@ -17,7 +17,7 @@ LIBPATH = os.path.join(_PKG, "_lib", "libtide_b200.so")
 F32, F16, BF16 = 0, 1, 2
 MODE_PER_TOKEN, MODE_BATCH_UNANIMOUS = 0, 1
 NO_EXIT = -1
-WORKSPACE_BYTES = 4 << 20
+WORKSPACE_BYTES = 8 << 20
 MAX_DECODE_ROWS = 16
 
 _c_p = ctypes.c_void_p

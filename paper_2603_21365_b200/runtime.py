@@ -141,6 +141,18 @@ def _check_bank(model, hidden_states, bank) -> None:
 
 def _stage_layers(hidden_states, needed: Sequence[int]):
     """Device tensors for the capture indices in `needed`, one common dtype."""
+    fast = {}
+    dt = None
+    for i in needed:
+        h = hidden_states[i]
+        if (type(h) is not torch.Tensor or not h.is_cuda or h.dim() != 2
+                or not h.is_contiguous() or (dt is not None and h.dtype != dt)):
+            break
+        dt = h.dtype
+        fast[i] = h
+    else:
+        if dt in (torch.float32, torch.float16, torch.bfloat16):
+            return fast, fast[needed[0]].device
     dev = None
     for h in hidden_states:
         if isinstance(h, torch.Tensor) and h.is_cuda:
@@ -163,6 +175,26 @@ def _stage_layers(hidden_states, needed: Sequence[int]):
     return out, dev
 
 
+_decode_plans: dict = {}
+
+
+def _decode_plan(bank, ckpts, code, dev):
+    """ctypes argument arrays of the decode launch (weight pointers, layers),
+    cached per (bank, checkpoints, dtype, device); rebuilt when a router or its
+    weights are replaced."""
+    routers = [bank.routers[k] for k in ckpts]
+    key = (id(bank), tuple(ckpts), code, dev.index)
+    hit = _decode_plans.get(key)
+    if hit is not None and all(r is h and r.w_down is wd and r.w_up is wu
+                               for r, (h, wd, wu) in zip(routers, hit[0])):
+        return hit[1]
+    ws_w = [device_weights(r, code, dev) for r in routers]
+    arrays = (N.ptr_array([w.data_ptr() for w, _ in ws_w]),
+              N.ptr_array([u.data_ptr() for _, u in ws_w]), N.i64_array(ckpts))
+    _decode_plans[key] = ([(r, r.w_down, r.w_up) for r in routers], arrays, ws_w, bank)
+    return arrays
+
+
 def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
                  staged=None, dev=None):
     """Exit map only (int64 CUDA tensor [n]); the hot path of posthoc_select."""
@@ -172,12 +204,11 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
         staged, dev = _stage_layers(hidden_states, [k + 1 for k in ckpts] + [L])
     final = staged[L]
     n, d = final.shape
-    exit_layers = torch.full((n,), NO_EXIT, dtype=torch.int64, device=dev)
     if not ckpts or n == 0:
-        return exit_layers
+        return torch.full((n,), NO_EXIT, dtype=torch.int64, device=dev)
     lib = N.load()
     s = D.stream_handle(dev)
-    ws = D.workspace(dev).data_ptr()
+    ws = D.workspace(dev, s).data_ptr()
     theta = float(np.float32(config.exit_threshold))
     eps = float(np.float32(bank.eps))
     code = D.dtype_code(final)
@@ -185,16 +216,15 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
     vec = 4 if code == N.F32 else 8
     decode_ok = d % vec == 0 and all(staged[k + 1].data_ptr() % 16 == 0 for k in ckpts)
     if n <= N.MAX_DECODE_ROWS and decode_ok:
-        ws_w = [device_weights(bank.routers[k], code, dev) for k in ckpts]
+        w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)
         mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
-        cnt = torch.empty(1, dtype=torch.int64, device=dev)
+        out = torch.empty((n,), dtype=torch.int64, device=dev)  # the kernel writes every row
         N.check(lib.tide_route_decode(
             N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
-            N.ptr_array([w.data_ptr() for w, _ in ws_w]),
-            N.ptr_array([u.data_ptr() for _, u in ws_w]), b, N.i64_array(ckpts), eps, theta,
-            int(config.k_min), mode, None, None, exit_layers.data_ptr(), cnt.data_ptr(), ws, s),
-            "tide_route_decode")
-        return exit_layers
+            w_arr, u_arr, b, l_arr, eps, theta, int(config.k_min), mode, None, None,
+            out.data_ptr(), None, ws, s), "tide_route_decode")
+        return out
+    exit_layers = torch.full((n,), NO_EXIT, dtype=torch.int64, device=dev)
     if config.mode == BATCH_UNANIMOUS:
         counts = torch.empty(2, dtype=torch.int64, device=dev)
         for k in ckpts:

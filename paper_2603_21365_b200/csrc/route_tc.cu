@@ -63,10 +63,21 @@ struct TcParams {
   int64_t* counts;
   Workspace* ws;
   unsigned long long* dbg;  // optional per-CTA timeline (globaltimer ns), 8 slots per CTA
-  int32_t prefetch;
-  uint32_t dbg_flags;       // experiments only: 1 = skip RMS reads, 2 = skip MMAs
 };
 
+// Cycle counters inside the streaming loops only in profiling builds
+// (-DTIDE_K1_PROFILE=1, tools/timeline.py): CS2R reads in the hot loops cost
+// issue slots the MMA warp shares.
+#ifndef TIDE_K1_PROFILE
+#define TIDE_K1_PROFILE 0
+#endif
+__device__ __forceinline__ long long pclk() {
+#if TIDE_K1_PROFILE
+  return clock64();
+#else
+  return 0;
+#endif
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -157,10 +168,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   if (warp == 0) {
     // ----------------------------------------------------------- producer
-    const uint64_t pol_h = (p.dbg_flags & 16u) ? 0x1000000000000000ull : policy_evict_first();
-    const uint64_t pol_w = (p.dbg_flags & 16u) ? 0x1000000000000000ull : policy_evict_last();
+    const uint64_t pol_h = policy_evict_first();
+    const uint64_t pol_w = policy_evict_last();
     int as = 0, aph = 0, wsl = 0, wph = 0;
-    long long pw_cyc = 0, p_begin = clock64();
+    long long pw_cyc = 0, p_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
       group_range(g, n, n32, NG, r0, r1);
@@ -172,33 +183,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         __syncwarp();
       }
       if (lane == 0) {
-        const int pd = p.prefetch;  // k-chunks of L2 prefetch ahead of the smem ring
-        if (!gathered && pd > 0)
-          for (int kc = 0; kc < pd && kc < p.nk; ++kc)
-            for (int t = 0; t < T; ++t) tma_prefetch_2d(&tm_h128, kc * 64, (int)(r0 + 128 * t));
         for (int kc = 0; kc < p.nk; ++kc) {
-          if (!gathered && pd > 0 && kc + pd < p.nk)
-            for (int t = 0; t < T; ++t)
-              tma_prefetch_2d(&tm_h128, (kc + pd) * 64, (int)(r0 + 128 * t));
           mbar_wait(&w_empty[wsl], wph ^ 1);
-          if (p.dbg_flags & 4u) {
-            mbar_arrive(&w_full[wsl]);
-          } else {
-            mbar_arrive_expect_tx(&w_full[wsl], p.wslot);
-            tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
-          }
+          mbar_arrive_expect_tx(&w_full[wsl], p.wslot);
+          tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
           if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
           for (int t = 0; t < T; ++t) {
-            const long long q0 = clock64();
+            const long long q0 = pclk();
             mbar_wait(&a_empty[as], aph ^ 1);
-            pw_cyc += clock64() - q0;
+            pw_cyc += pclk() - q0;
             uint8_t* dst = sA + (size_t)as * kASlotBytes;
             const int64_t rb = r0 + (int64_t)t * 128;
             const int rows_in = (int)((r1 - rb) < 128 ? (r1 - rb) : 128);
-            if (p.dbg_flags & 4u) {
-              mbar_arrive(&a_full[as]);
-            } else if (!gathered) {
-              if (rows_in == 128 || (p.dbg_flags & 32u)) {
+            if (!gathered) {
+              if (rows_in == 128) {
                 mbar_arrive_expect_tx(&a_full[as], kASlotBytes);
                 tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
               } else {
@@ -232,7 +230,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
       }
     }
-    if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[18] = pw_cyc; dbg[19] = clock64() - p_begin; }
+    if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[18] = pw_cyc; dbg[19] = pclk() - p_begin; }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (warp-uniform state -> uniform registers);
@@ -240,7 +238,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // advanced by +2 (32 bytes >> 4) per K=16 step.
     int as = 0, aph = 0, wsl = 0, wph = 0;
     uint32_t accph = 0;
-    long long wait_cyc = 0, t_begin = clock64();
+    long long wait_cyc = 0, t_begin = pclk();
     const uint64_t desc_hi = sw128_kmajor_desc(0);
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
@@ -249,74 +247,36 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
       tc_fence_after();
       for (int kc = 0; kc < p.nk; ++kc) {
-        const long long w0 = clock64();
+        const long long w0 = pclk();
         mbar_wait(&w_full[wsl], wph);
-        wait_cyc += clock64() - w0;
+        wait_cyc += pclk() - w0;
         const uint64_t bdesc = desc_hi | (uint64_t)((smem_u32(sW + (size_t)wsl * p.wslot) & 0x3FFFFu) >> 4);
-        if (p.dbg_flags & 64u) {
-          // batched: wait every tile's slot, one fence, all MMAs, then commits
-          int slot[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            if (t < T) {
-              slot[t] = as;
-              mbar_wait(&a_full[as], aph);
-              if (++as == p.na) { as = 0; aph ^= 1; }
-            }
-          }
+        // per tile: its slot is released as soon as ITS 4 MMAs retire
+        for (int t = 0; t < T; ++t) {
+          const long long w1 = pclk();
+          mbar_wait(&a_full[as], aph);
+          wait_cyc += pclk() - w1;
           tc_fence_after();
           if (elect_one()) {
+            const uint64_t adesc =
+                desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * kASlotBytes) & 0x3FFFFu) >> 4);
+            const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              if (t < T) {
-                const uint64_t adesc =
-                    desc_hi | (uint64_t)((smem_u32(sA + (size_t)slot[t] * kASlotBytes) & 0x3FFFFu) >> 4);
-                const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  if (!(p.dbg_flags & 2u))
-                    tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
-              }
-            }
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              if (t < T) {
-                tc_commit(&a_empty[slot[t]]);
-                if (kc == p.nk - 1) tc_commit(&t_full[t]);
-              }
-            }
-            tc_commit(&w_empty[wsl]);
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+            tc_commit(&a_empty[as]);
+            if (kc == p.nk - 1) tc_commit(&t_full[t]);
           }
-        } else {
-          // per tile: its slot is released as soon as ITS 4 MMAs retire
-          const uint32_t idesc = (p.dbg_flags & 128u) ? f16_idesc(kBF16 ? 1 : 0, 128, 64) : p.idesc;
-          const int ksteps = (p.dbg_flags & 256u) ? 2 : 4;
-          for (int t = 0; t < T; ++t) {
-            const long long w1 = clock64();
-            mbar_wait(&a_full[as], aph);
-            wait_cyc += clock64() - w1;
-            tc_fence_after();
-            if (elect_one()) {
-              const uint64_t adesc =
-                  desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * kASlotBytes) & 0x3FFFFu) >> 4);
-              const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
-              for (int k = 0; k < ksteps; ++k)
-                if (!(p.dbg_flags & 2u))
-                  tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, idesc, (kc | k) != 0);
-              tc_commit(&a_empty[as]);
-              if (kc == p.nk - 1) tc_commit(&t_full[t]);
-            }
-            __syncwarp();
-            if (++as == p.na) { as = 0; aph ^= 1; }
-          }
-          if (elect_one()) tc_commit(&w_empty[wsl]);
+          __syncwarp();
+          if (++as == p.na) { as = 0; aph ^= 1; }
         }
+        if (elect_one()) tc_commit(&w_empty[wsl]);
         __syncwarp();
         if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
       }
       accph ^= (1u << T) - 1u;
     }
-    if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = clock64() - t_begin; }
+    if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = pclk() - t_begin; }
   } else if (warp <= 9) {
     // ----------------------------------------------------------- RMS + epilogue
     // Two sets of 4 warps: set 0 (warps 2-5) owns tiles 0-1, set 1 (warps 6-9)
@@ -328,7 +288,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t swz = (uint32_t)(row & 7);
     int as = 0, aph = 0, gi = 0;
     uint32_t accph = 0;
-    long long sw_cyc = 0, s_begin = clock64();
+    long long sw_cyc = 0, s_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
       group_range(g, n, n32, NG, r0, r1);
@@ -343,19 +303,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (t < T && (t >> 1) != wset) {
             if (++as == p.na) { as = 0; aph ^= 1; }
           } else if (t < T) {
-            const long long s0 = clock64();
+            const long long s0 = pclk();
             mbar_wait(&a_full[as], aph);
-            sw_cyc += clock64() - s0;
+            sw_cyc += pclk() - s0;
             const uint8_t* rp = sA + (size_t)as * kASlotBytes + row * 128;
             uint4 u[8];
-            if (p.dbg_flags & 1u) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) u[j] = make_uint4(0, 0, 0, 0);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
-            }
+            for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_empty[as]);
 #pragma unroll
@@ -377,7 +331,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         }
       }
-      if (dbg && warp == 2 && lane == 0) { dbg[2] = gtimer(); dbg[20] = sw_cyc; dbg[21] = clock64() - s_begin; }
+      if (dbg && warp == 2 && lane == 0) { dbg[2] = gtimer(); dbg[20] = sw_cyc; dbg[21] = pclk() - s_begin; }
       float ssum[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -398,21 +352,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const bool valid = r < r1;
           const float sq = t == 0 ? ssum[0] : t == 1 ? ssum[1] : t == 2 ? ssum[2] : ssum[3];
           const float scale = rms_scale(sq, p.inv_d, p.eps);
-          const f32x2 scale2 = pack2(scale, scale);
-          const float nsl = -scale * 1.4426950408889634f;
-          const f32x2 nsl2 = pack2(nsl, nsl);
+          const float hs = 0.5f * scale;  // exact (power of two)
+          const f32x2 hs2 = pack2(hs, hs);
           f32x2 acc2 = 0ull;
           const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(t * p.bp);
-          for (int c0 = 0; c0 < p.b; c0 += 32) {
-            uint32_t v[32];
-            tmem_ld32(taddr + (uint32_t)c0, v);
-            tmem_ld_wait();
+          // 32 accumulator columns per tcgen05.ld, two in flight: the next
+          // chunk's TMEM read overlaps this chunk's SiLU / w_up math.
+          auto consume = [&](const uint32_t (&v)[32], int c0) {
             if (c0 + 32 <= p.b) {
 #pragma unroll
               for (int jj = 0; jj < 32; jj += 4) {
                 const float4 w4 = *reinterpret_cast<const float4*>(sWup + c0 + jj);
-                const f32x2 s01 = silu2_fast(pack2u(v[jj], v[jj + 1]), scale2, nsl2);
-                const f32x2 s23 = silu2_fast(pack2u(v[jj + 2], v[jj + 3]), scale2, nsl2);
+                const f32x2 s01 = silu2_tanh(fmul2(pack2u(v[jj], v[jj + 1]), hs2));
+                const f32x2 s23 = silu2_tanh(fmul2(pack2u(v[jj + 2], v[jj + 3]), hs2));
                 acc2 = ffma2(pack2(w4.x, w4.y), s01, acc2);
                 acc2 = ffma2(pack2(w4.z, w4.w), s23, acc2);
               }
@@ -422,10 +374,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 if (c0 + jj < p.b) {
                   const float w0 = sWup[c0 + jj];
                   const float w1 = (c0 + jj + 1 < p.b) ? sWup[c0 + jj + 1] : 0.0f;
-                  const f32x2 s01 = silu2_fast(pack2u(v[jj], v[jj + 1]), scale2, nsl2);
+                  const f32x2 s01 = silu2_tanh(fmul2(pack2u(v[jj], v[jj + 1]), hs2));
                   acc2 = ffma2(pack2(w0, w1), s01, acc2);
                 }
               }
+            }
+          };
+          uint32_t va[32], vb[32];
+          tmem_ld32(taddr, va);
+          tmem_ld_wait_regs(va);
+          for (int c0 = 0; c0 < p.b; c0 += 64) {
+            const bool has_b = c0 + 32 < p.b;
+            if (has_b) tmem_ld32(taddr + (uint32_t)(c0 + 32), vb);
+            consume(va, c0);
+            if (has_b) {
+              tmem_ld_wait_regs(vb);
+              if (c0 + 64 < p.b) tmem_ld32(taddr + (uint32_t)(c0 + 64), va);
+              consume(vb, c0 + 32);
+              if (c0 + 64 < p.b) tmem_ld_wait_regs(va);
             }
           }
           tc_fence_before();
@@ -460,7 +426,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int64_t r0, r1;
       group_range(g, n, n32, NG, r0, r1);
       const int par = gi & 1;
-      mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
+      mbar_wait_sleep(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
       __syncwarp();
       if (lane == 0) mbar_arrive(&m_empty[par]);
@@ -684,14 +650,6 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.counts = a.counts;
   p.ws = reinterpret_cast<Workspace*>(a.workspace);
   p.dbg = g_dbg;
-  {
-    static const char* pf = getenv("TIDE_PREFETCH");
-    p.prefetch = pf ? atoi(pf) : 0;  // L2 prefetch measured slower: off by default
-  }
-  {
-    static const char* env = getenv("TIDE_DEBUG_FLAGS");
-    p.dbg_flags = env ? (uint32_t)atoi(env) : 0u;
-  }
 
   CUtensorMap tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4;
   const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);

@@ -146,6 +146,16 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int N, int iters, Out*
       }
       if (opt & 4) { for (int i = iters; i < iters + 8; ++i) { const int s = i % 8; mb_wait(&bars[s], (phs >> s) & 1); phs ^= (1u << s); } }
       else { commit(&bars[31]); mb_wait(&bars[31], 0); }
+    } else if (mode == 13) {
+      // commit-only throughput: one commit per slot into a ring of 9, waiting 8 behind
+      uint32_t phs = 0;
+      for (int i = 0; i < iters; ++i) {
+        const int s = i % 9;
+        if (i >= 9) { mb_wait(&bars[s], (phs >> s) & 1); phs ^= (1u << s); }
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        commit(&bars[s]);
+      }
+      for (int i = iters; i < iters + 9; ++i) { const int s = i % 9; mb_wait(&bars[s], (phs >> s) & 1); phs ^= (1u << s); }
     } else if (mode == 5) {
       for (int i = 0; i < iters; ++i)
         for (int k = 0; k < 4; ++k) mma(tmem + (i & 1) * 256, desc(a0 + 32 * k), desc(b0 + 32 * k), idesc, k != 0);
@@ -168,7 +178,12 @@ int main() {
   Out* d; CK(cudaMalloc(&d, sizeof(Out) * 148));
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   const char* names[] = {"mbarrier ping-pong (round trip)", "commit+wait, no MMA", "4 MMA + commit + wait (latency)", "4 MMA/commit, ring of 9 (thru)", "8 MMA/commit, ring of 9 (thru)", "MMA issue only (per 4 MMAs)", "4 indep-acc MMA/commit, ring 9", "16 MMA (4acc x 4k)/commit, ring 9", "mode3 without fence", "mode3 without wait", "mode3 no commit/wait", "mode3 again"};
-  for (int opt : {0, 4, 5, 16, 20, 21, 48, 52, 53}) for (int nthr : {64, 256}) {
+  for (int mode : {0, 1, 2, 3, 13}) {
+    probe<<<148, 64, 220 * 1024>>>(mode, 128, 1000, d, 0); CK(cudaDeviceSynchronize());
+    Out o; CK(cudaMemcpy(&o, d, sizeof(Out), cudaMemcpyDeviceToHost));
+    printf("mode %2d %-40s: %lld cyc/iter\n", mode, mode == 13 ? "commit-only ring of 9 (thru)" : names[mode], o.cyc[0]);
+  }
+  for (int opt : {0, 2, 5, 7}) for (int nthr : {64}) {
     const int N = 128;
     const int iters = 1000;
     probe<<<148, nthr, 220 * 1024>>>(12, N, iters, d, opt);

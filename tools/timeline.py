@@ -11,7 +11,7 @@ g = np.random.Generator(np.random.PCG64(202))
 orr = O.make_router(d, b, 3, g)
 router = P.Router(3, orr.w_down, orr.w_up)
 h = torch.randn((n, d), device="cuda").to(torch.bfloat16)
-lib = N.load()
+lib = N.load(os.environ['TIDE_PROBE_LIB']) if os.environ.get('TIDE_PROBE_LIB') else N.load()
 lib.tide_debug_timeline.argtypes = [ctypes.c_void_p]
 dbg = torch.zeros(148 * 24, dtype=torch.int64, device="cuda")
 for it in range(4):

@@ -46,7 +46,7 @@ struct TcParams {
   int64_t n_host;
   const int64_t* n_dev;
   int64_t rows_total;
-  int32_t d, b, npad, bp, tpg, nk, na, nw;
+  int32_t d, b, npad, bp, tpg, nk, na, nw, nx;
   uint32_t idesc, tmem_cols, wslot;
   uint32_t off_a, off_wup, off_bar, off_words, off_ids, off_tmem;
   const int64_t* row_idx;
@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const uint32_t tag = launch_tag(p.ws);
   const bool gathered = p.row_idx != nullptr;
   const bool need_scan = p.exit_idx || p.cont_idx || p.counts;
+  auto bounds = [&](int64_t g, int64_t& r0, int64_t& r1) { group_range(g, n, n32, NG, r0, r1); };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_w);
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     long long pw_cyc = 0, p_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      bounds(g, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       if (gathered) {
         __syncwarp();
@@ -183,51 +184,65 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         __syncwarp();
       }
       if (lane == 0) {
-        for (int kc = 0; kc < p.nk; ++kc) {
+        auto load_w = [&](int kc) {
           mbar_wait(&w_empty[wsl], wph ^ 1);
           mbar_arrive_expect_tx(&w_full[wsl], p.wslot);
           tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
           if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
-          for (int t = 0; t < T; ++t) {
-            const long long q0 = pclk();
-            mbar_wait(&a_empty[as], aph ^ 1);
-            pw_cyc += pclk() - q0;
-            uint8_t* dst = sA + (size_t)as * kASlotBytes;
-            const int64_t rb = r0 + (int64_t)t * 128;
-            const int rows_in = (int)((r1 - rb) < 128 ? (r1 - rb) : 128);
-            if (!gathered) {
-              if (rows_in == 128) {
-                mbar_arrive_expect_tx(&a_full[as], kASlotBytes);
-                tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
-              } else {
-                // ragged tail: greedy 64/32/16-row boxes (16-row boxes stream poorly)
-                const int rr = (rows_in + kGran - 1) / kGran * kGran;
-                mbar_arrive_expect_tx(&a_full[as], (uint32_t)(rr * 128));
-                int off = 0;
-                if (rr - off >= 64) {
-                  tma_load_2d(dst, &tm_h64, &a_full[as], kc * 64, (int)rb, pol_h);
-                  off += 64;
-                }
-                if (rr - off >= 32) {
-                  tma_load_2d(dst + off * 128, &tm_h32b, &a_full[as], kc * 64, (int)(rb + off), pol_h);
-                  off += 32;
-                }
-                if (rr - off >= 16) {
-                  tma_load_2d(dst + off * 128, &tm_h32, &a_full[as], kc * 64, (int)(rb + off), pol_h);
-                  off += 16;
-                }
-              }
+        };
+        auto load_a = [&](int kc, int t) {
+          const long long q0 = pclk();
+          mbar_wait(&a_empty[as], aph ^ 1);
+          pw_cyc += pclk() - q0;
+          uint8_t* dst = sA + (size_t)as * kASlotBytes;
+          const int64_t rb = r0 + (int64_t)t * 128;
+          const int rows_in = (int)((r1 - rb) < 128 ? (r1 - rb) : 128);
+          if (!gathered) {
+            if (rows_in == 128) {
+              mbar_arrive_expect_tx(&a_full[as], kASlotBytes);
+              tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
             } else {
-              const int ng4 = (rows_in + 3) / 4;
-              mbar_arrive_expect_tx(&a_full[as], ng4 * 512);
-              const uint32_t* id = ids + t * 128;
-              for (int q = 0; q < ng4; ++q)
-                tma_gather4(dst + q * 512, &tm_g4, &a_full[as], kc * 64, (int)id[4 * q],
-                            (int)id[4 * q + 1], (int)id[4 * q + 2], (int)id[4 * q + 3], pol_h);
+              // ragged tail: greedy 64/32/16-row boxes (16-row boxes stream poorly)
+              const int rr = (rows_in + kGran - 1) / kGran * kGran;
+              mbar_arrive_expect_tx(&a_full[as], (uint32_t)(rr * 128));
+              int off = 0;
+              if (rr - off >= 64) {
+                tma_load_2d(dst, &tm_h64, &a_full[as], kc * 64, (int)rb, pol_h);
+                off += 64;
+              }
+              if (rr - off >= 32) {
+                tma_load_2d(dst + off * 128, &tm_h32b, &a_full[as], kc * 64, (int)(rb + off), pol_h);
+                off += 32;
+              }
+              if (rr - off >= 16) {
+                tma_load_2d(dst + off * 128, &tm_h32, &a_full[as], kc * 64, (int)(rb + off), pol_h);
+                off += 16;
+              }
             }
-            if (++as == p.na) { as = 0; aph ^= 1; }
+          } else {
+            const int ng4 = (rows_in + 3) / 4;
+            mbar_arrive_expect_tx(&a_full[as], ng4 * 512);
+            const uint32_t* id = ids + t * 128;
+            for (int q = 0; q < ng4; ++q)
+              tma_gather4(dst + q * 512, &tm_g4, &a_full[as], kc * 64, (int)id[4 * q],
+                          (int)id[4 * q + 1], (int)id[4 * q + 2], (int)id[4 * q + 3], pol_h);
           }
+          if (++as == p.na) { as = 0; aph ^= 1; }
+        };
+        // phase 1 (K-outer): chunk kc's W slot feeds all T tiles
+        const int P1 = p.nk - p.nx;
+        for (int kc = 0; kc < P1; ++kc) {
+          load_w(kc);
+          for (int t = 0; t < T; ++t) load_a(kc, t);
         }
+        // phase 2 (tile-major over the last nx chunks, whose W slots stay
+        // resident): tile t's accumulator completes while later tiles still
+        // stream, so its epilogue overlaps the tail of the stream
+        for (int t = 0; t < T; ++t)
+          for (int j = 0; j < p.nx; ++j) {
+            if (t == 0) load_w(P1 + j);
+            load_a(P1 + j, t);
+          }
       }
     }
     if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[18] = pw_cyc; dbg[19] = pclk() - p_begin; }
@@ -242,46 +257,68 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint64_t desc_hi = sw128_kmajor_desc(0);
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      bounds(g, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
       tc_fence_after();
-      for (int kc = 0; kc < p.nk; ++kc) {
+      auto mma_slot = [&](int kc, int t, uint64_t bdesc) {
+        const long long w1 = pclk();
+        mbar_wait(&a_full[as], aph);
+        wait_cyc += pclk() - w1;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t adesc =
+              desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * kASlotBytes) & 0x3FFFFu) >> 4);
+          const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+          // the slot is released as soon as ITS 4 MMAs retire
+          tc_commit(&a_empty[as]);
+          if (kc == p.nk - 1) tc_commit(&t_full[t]);
+        }
+        __syncwarp();
+        if (++as == p.na) { as = 0; aph ^= 1; }
+      };
+      auto wdesc = [&](int slot) {
+        return desc_hi | (uint64_t)((smem_u32(sW + (size_t)slot * p.wslot) & 0x3FFFFu) >> 4);
+      };
+      // phase 1: K-outer
+      const int P1 = p.nk - p.nx;
+      for (int kc = 0; kc < P1; ++kc) {
         const long long w0 = pclk();
         mbar_wait(&w_full[wsl], wph);
         wait_cyc += pclk() - w0;
-        const uint64_t bdesc = desc_hi | (uint64_t)((smem_u32(sW + (size_t)wsl * p.wslot) & 0x3FFFFu) >> 4);
-        // per tile: its slot is released as soon as ITS 4 MMAs retire
-        for (int t = 0; t < T; ++t) {
-          const long long w1 = pclk();
-          mbar_wait(&a_full[as], aph);
-          wait_cyc += pclk() - w1;
-          tc_fence_after();
-          if (elect_one()) {
-            const uint64_t adesc =
-                desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * kASlotBytes) & 0x3FFFFu) >> 4);
-            const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc_mma_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
-            tc_commit(&a_empty[as]);
-            if (kc == p.nk - 1) tc_commit(&t_full[t]);
-          }
-          __syncwarp();
-          if (++as == p.na) { as = 0; aph ^= 1; }
-        }
+        const uint64_t bdesc = wdesc(wsl);
+        for (int t = 0; t < T; ++t) mma_slot(kc, t, bdesc);
         if (elect_one()) tc_commit(&w_empty[wsl]);
         __syncwarp();
         if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
       }
+      // phase 2: tile-major over the last nx chunks (W slots wsl .. wsl+nx-1)
+      for (int t = 0; t < T; ++t) {
+        int sl = wsl, ph = wph;
+        for (int j = 0; j < p.nx; ++j) {
+          if (t == 0) mbar_wait(&w_full[sl], ph);
+          mma_slot(P1 + j, t, wdesc(sl));
+          if (t == T - 1) {
+            if (elect_one()) tc_commit(&w_empty[sl]);
+            __syncwarp();
+          }
+          if (++sl == p.nw) { sl = 0; ph ^= 1; }
+        }
+      }
+      for (int j = 0; j < p.nx; ++j)
+        if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
       accph ^= (1u << T) - 1u;
     }
     if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = pclk() - t_begin; }
   } else if (warp <= 9) {
     // ----------------------------------------------------------- RMS + epilogue
-    // Two sets of 4 warps: set 0 (warps 2-5) owns tiles 0-1, set 1 (warps 6-9)
-    // tiles 2-3 — both the RMS reads of those tiles' A slots and their
-    // epilogues, so the post-stream tail is split across 8 warps.
+    // Two sets of 4 warps: set 0 (warps 2-5) owns tiles 0 and 2, set 1
+    // (warps 6-9) tiles 1 and 3 — both the RMS reads of those tiles' A slots
+    // and their epilogues.  Tiles complete in order 0,1,2,3 (phase 2), so the
+    // sets alternate and each epilogue overlaps the stream of later tiles.
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int wset = (warp - 2) >> 2;
     const int row = 32 * q + lane;
@@ -291,58 +328,53 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     long long sw_cyc = 0, s_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      bounds(g, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       // sum of squares of this thread's row, per tile, from the swizzled A slots
       f32x2 ss[4][2];
 #pragma unroll
       for (int t = 0; t < 4; ++t) ss[t][0] = ss[t][1] = 0ull;
-      for (int kc = 0; kc < p.nk; ++kc) {
+      auto rms_slot = [&](int t, f32x2 (&acc)[2]) {
+        if ((t & 1) == wset) {
+          const long long s0 = pclk();
+          mbar_wait(&a_full[as], aph);
+          sw_cyc += pclk() - s0;
+          const uint8_t* rp = sA + (size_t)as * kASlotBytes + row * 128;
+          uint4 u[8];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          if (t < T && (t >> 1) != wset) {
-            if (++as == p.na) { as = 0; aph ^= 1; }
-          } else if (t < T) {
-            const long long s0 = pclk();
-            mbar_wait(&a_full[as], aph);
-            sw_cyc += pclk() - s0;
-            const uint8_t* rp = sA + (size_t)as * kASlotBytes + row * 128;
-            uint4 u[8];
+          for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_empty[as]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&a_empty[as]);
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                f32x2 x;
-                if (kBF16) {
-                  x = pack2u(w[e] << 16, w[e] & 0xFFFF0000u);
-                } else {
-                  const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
-                  x = pack2(f2.x, f2.y);
-                }
-                ss[t][e & 1] = ffma2(x, x, ss[t][e & 1]);
+            for (int e = 0; e < 4; ++e) {
+              f32x2 x;
+              if (kBF16) {
+                x = pack2u(w[e] << 16, w[e] & 0xFFFF0000u);
+              } else {
+                const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+                x = pack2(f2.x, f2.y);
               }
+              acc[e & 1] = ffma2(x, x, acc[e & 1]);
             }
-            if (++as == p.na) { as = 0; aph ^= 1; }
           }
         }
-      }
-      if (dbg && warp == 2 && lane == 0) { dbg[2] = gtimer(); dbg[20] = sw_cyc; dbg[21] = pclk() - s_begin; }
-      float ssum[4];
+        if (++as == p.na) { as = 0; aph ^= 1; }
+      };
+      // same slot order as the producer: phase 1 K-outer, phase 2 tile-major
+      const int P1 = p.nk - p.nx;
+      for (int kc = 0; kc < P1; ++kc) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        float a0, a1, b0, b1;
-        unpack2(ss[t][0], a0, a1);
-        unpack2(ss[t][1], b0, b1);
-        ssum[t] = (a0 + b0) + (a1 + b1);
+        for (int t = 0; t < 4; ++t)
+          if (t < T) rms_slot(t, ss[t]);
       }
       const int par = gi & 1;
       mbar_wait(&m_empty[par], (((uint32_t)gi >> 1) & 1u) ^ 1u);
-      for (int t = 2 * wset; t < 2 * wset + 2; ++t) {
+      // epilogue of one tile: tcgen05.ld the row's b pre-activations, scale,
+      // SiLU, dot w_up, f64 sigmoid, strict threshold, ballot -> words
+      auto epilogue = [&](int t, const f32x2 (&acc_ss)[2]) {
         uint32_t bal = 0;
         if (t < T) {
           mbar_wait(&t_full[t], (accph >> t) & 1u);
@@ -350,7 +382,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (dbg && warp == 2 && lane == 0) dbg[8 + 2 * t] = gtimer();
           const int64_t r = r0 + (int64_t)t * 128 + row;
           const bool valid = r < r1;
-          const float sq = t == 0 ? ssum[0] : t == 1 ? ssum[1] : t == 2 ? ssum[2] : ssum[3];
+          float sa0, sa1, sb0, sb1;
+          unpack2(acc_ss[0], sa0, sa1);
+          unpack2(acc_ss[1], sb0, sb1);
+          const float sq = (sa0 + sb0) + (sa1 + sb1);
           const float scale = rms_scale(sq, p.inv_d, p.eps);
           const float hs = 0.5f * scale;  // exact (power of two)
           const f32x2 hs2 = pack2(hs, hs);
@@ -412,6 +447,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           bal = __ballot_sync(0xffffffffu, ex);
         }
         if (lane == 0) words[par * 16 + t * 4 + q] = bal;
+      };
+      // phase 2: this set's tiles in completion order; each tile's epilogue
+      // runs while the other set's next tile streams
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t < T)
+          for (int j = 0; j < p.nx; ++j) rms_slot(t, ss[t]);
+        if ((t & 1) == wset) {
+          if (t == wset && dbg && warp == 2 && lane == 0) { dbg[2] = gtimer(); dbg[20] = sw_cyc; dbg[21] = pclk() - s_begin; }
+          epilogue(t, ss[t]);
+        }
       }
       accph ^= (1u << T) - 1u;
       __syncwarp();
@@ -424,7 +470,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int gi = 0;
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      bounds(g, r0, r1);
       const int par = gi & 1;
       mbar_wait_sleep(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
@@ -624,6 +670,7 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.nk = nk;
   p.na = na;
   p.nw = nw;
+  p.nx = std::min(nw, nk);  // tile-major tail chunks (W slots kept resident)
   p.idesc = f16_idesc(a.dtype == TIDE_BF16 ? 1 : 0, 128, npad);
   p.tmem_cols = (uint32_t)cols;
   p.wslot = wslot;

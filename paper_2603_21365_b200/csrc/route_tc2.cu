@@ -35,6 +35,16 @@ constexpr int kMaxNW2 = 8;
 constexpr int kASlot2 = 128 * 128;
 constexpr int kGran2 = 16;
 
+#ifndef TIDE_K1_PROFILE
+#define TIDE_K1_PROFILE 0
+#endif
+__device__ __forceinline__ long long pclk2() {
+#if TIDE_K1_PROFILE
+  return clock64();
+#else
+  return 0;
+#endif
+}
 __device__ __forceinline__ unsigned long long gtimer2() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -133,7 +143,6 @@ struct Tc2Params {
   int64_t* counts;
   Workspace* ws;
   unsigned long long* dbg;
-  uint32_t dbg_flags;  // experiments: 2 = skip MMAs, 8 = no a_ready forwarding (peer RMS unsynchronised)
 };
 
 // Pair-group g of NGp covers units [g*U/NGp, (g+1)*U/NGp) (kGran2 rows each);
@@ -237,9 +246,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 
   if (warp == 0) {
     // ----------------------------------------------------------- producer (both CTAs)
-    long long pw_cyc = 0, p_begin = clock64();
-    const uint64_t pol_h = (p.dbg_flags & 16u) ? 0x1000000000000000ull : policy_evict_first();
-    const uint64_t pol_w = (p.dbg_flags & 16u) ? 0x1000000000000000ull : policy_evict_last();
+    long long pw_cyc = 0, p_begin = pclk2();
+    const uint64_t pol_h = policy_evict_first();
+    const uint64_t pol_w = policy_evict_last();
     int as = 0, aph = 0, wsl = 0, wph = 0;
     for (int64_t g = pid; g < NGp; g += P) {
       int64_t r0, r1, o0, o1;
@@ -259,16 +268,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                       rank * (p.npad / 2), pol_w);
           if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
           for (int t = 0; t < T; ++t) {
-            const long long q0 = clock64();
+            const long long q0 = pclk2();
             mbar_wait(&a_empty[as], aph ^ 1);
-            pw_cyc += clock64() - q0;
+            pw_cyc += pclk2() - q0;
             uint8_t* dst = sA + (size_t)as * kASlot2;
             uint64_t* abar = &a_land[as];
             auto expect = [&](uint32_t bytes) { mbar_arrive_expect_tx(abar, bytes); };
             const int64_t rb = r0 + (int64_t)t * 128;
             const int rows_in = (int)std::max<int64_t>(0, std::min<int64_t>(128, r1 - rb));
             if (!gathered) {
-              if (rows_in == 128 || ((p.dbg_flags & 32u) && rows_in > 0)) {
+              if (rows_in == 128) {
                 expect(kASlot2);
                 tma_load_2d(dst, &tm_h128, abar, kc * 64, (int)rb, pol_h);
               } else {
@@ -299,11 +308,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
       }
     }
-    if (dbg && lane == 0) { dbg[1] = gtimer2(); dbg[18] = pw_cyc; dbg[19] = clock64() - p_begin; }
+    if (dbg && lane == 0) { dbg[1] = gtimer2(); dbg[18] = pw_cyc; dbg[19] = pclk2() - p_begin; }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer (leader only)
     if (leader) {
-      long long wait_cyc = 0, t_begin = clock64();
+      long long wait_cyc = 0, t_begin = pclk2();
       int as = 0, aph = 0, wsl = 0, wph = 0;
       uint32_t accph = 0;
       const uint64_t desc_hi = sw128_kmajor_desc(0);
@@ -316,17 +325,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         for (int kc = 0; kc < p.nk; ++kc) {
           // per tile: wait both CTAs' A halves, one fence, 4 K-steps, commit -> the
           // slot is released as soon as ITS MMAs retire (not the whole k-chunk's)
-          const long long w0 = clock64();
+          const long long w0 = pclk2();
           mbar_wait(&w_land[wsl], wph);
           mbar_wait(&w_peer[wsl], wph);
-          wait_cyc += clock64() - w0;
+          wait_cyc += pclk2() - w0;
           const uint64_t bdesc =
               desc_hi | (uint64_t)((smem_u32(sW + (size_t)wsl * p.wslot) & 0x3FFFFu) >> 4);
           for (int t = 0; t < T; ++t) {
-            const long long w1 = clock64();
+            const long long w1 = pclk2();
             mbar_wait(&a_land[as], aph);
             mbar_wait(&a_peer[as], aph);
-            wait_cyc += clock64() - w1;
+            wait_cyc += pclk2() - w1;
             tc_fence_after();
             if (elect_one()) {
               const uint64_t adesc =
@@ -334,8 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                if (!(p.dbg_flags & 2u))
-                  mma2_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+                mma2_f16(dt, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
               commit2_both(&a_empty[as]);
               if (kc == p.nk - 1) commit2_both(&t_full[t]);
             }
@@ -348,7 +356,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
         accph ^= (1u << T) - 1u;
       }
-      if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = clock64() - t_begin; }
+      if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = pclk2() - t_begin; }
     } else if (lane == 0) {
       // peer: forward "my half landed" to the leader, slot by slot, in MMA order
       int as = 0, aph = 0, wsl = 0, wph = 0;
@@ -377,7 +385,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     uint64_t* ready = a_land;
     int as = 0, aph = 0, gi = 0;
     uint32_t accph = 0;
-    long long sw_cyc = 0, s_begin = clock64();
+    long long sw_cyc = 0, s_begin = pclk2();
     for (int64_t g = pid; g < NGp; g += P) {
       int64_t r0, r1, o0, o1;
       half_range(g, n, U, NGp, rank, r0, r1, o0, o1);
@@ -391,9 +399,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           if (t < T && (t >> 1) != wset) {
             if (++as == p.na) { as = 0; aph ^= 1; }
           } else if (t < T) {
-            const long long s0 = clock64();
+            const long long s0 = pclk2();
             mbar_wait(&ready[as], aph);
-            sw_cyc += clock64() - s0;
+            sw_cyc += pclk2() - s0;
             const uint8_t* rp = sA + (size_t)as * kASlot2 + row * 128;
             uint4 u[8];
 #pragma unroll
@@ -419,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           }
         }
       }
-      if (dbg && warp == 2 && lane == 0) { dbg[2] = gtimer2(); dbg[20] = sw_cyc; dbg[21] = clock64() - s_begin; }
+      if (dbg && warp == 2 && lane == 0) { dbg[2] = gtimer2(); dbg[20] = sw_cyc; dbg[21] = pclk2() - s_begin; }
       float ssum[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -439,9 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           const bool valid = r < r1;
           const float sq = t == 0 ? ssum[0] : t == 1 ? ssum[1] : t == 2 ? ssum[2] : ssum[3];
           const float scale = rms_scale(sq, p.inv_d, p.eps);
-          const f32x2 scale2 = pack2(scale, scale);
-          const float nsl = -scale * 1.4426950408889634f;
-          const f32x2 nsl2 = pack2(nsl, nsl);
+          const float hs = 0.5f * scale;  // exact (power of two)
+          const f32x2 hs2 = pack2(hs, hs);
           f32x2 acc2 = 0ull;
           const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(t * p.bp);
           for (int c0 = 0; c0 < p.b; c0 += 32) {
@@ -452,8 +459,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 #pragma unroll
               for (int jj = 0; jj < 32; jj += 4) {
                 const float4 w4 = *reinterpret_cast<const float4*>(sWup + c0 + jj);
-                const f32x2 s01 = silu2_fast(pack2u(v[jj], v[jj + 1]), scale2, nsl2);
-                const f32x2 s23 = silu2_fast(pack2u(v[jj + 2], v[jj + 3]), scale2, nsl2);
+                const f32x2 s01 = silu2_tanh(fmul2(pack2u(v[jj], v[jj + 1]), hs2));
+                const f32x2 s23 = silu2_tanh(fmul2(pack2u(v[jj + 2], v[jj + 3]), hs2));
                 acc2 = ffma2(pack2(w4.x, w4.y), s01, acc2);
                 acc2 = ffma2(pack2(w4.z, w4.w), s23, acc2);
               }
@@ -463,7 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 if (c0 + jj < p.b) {
                   const float w0 = sWup[c0 + jj];
                   const float w1 = (c0 + jj + 1 < p.b) ? sWup[c0 + jj + 1] : 0.0f;
-                  const f32x2 s01 = silu2_fast(pack2u(v[jj], v[jj + 1]), scale2, nsl2);
+                  const f32x2 s01 = silu2_tanh(fmul2(pack2u(v[jj], v[jj + 1]), hs2));
                   acc2 = ffma2(pack2(w0, w1), s01, acc2);
                 }
               }
@@ -617,10 +624,6 @@ int route_tc2_launch(const RouteArgs& a, cudaStream_t stream) {
   p.counts = a.counts;
   p.ws = reinterpret_cast<Workspace*>(a.workspace);
   p.dbg = g_dbg;
-  {
-    static const char* env = getenv("TIDE_DEBUG_FLAGS");
-    p.dbg_flags = env ? (uint32_t)atoi(env) : 0u;
-  }
 
   CUtensorMap tm_h128, tm_h64, tm_h32, tm_h16, tm_w, tm_g4;
   const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);

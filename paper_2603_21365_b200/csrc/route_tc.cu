@@ -330,11 +330,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int64_t r0, r1;
       bounds(g, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
-      // sum of squares of this thread's row, per tile, from the swizzled A slots
-      f32x2 ss[4][2];
+      // sum of squares of this thread's row for each of its two tiles
+      // (t = wset, wset + 2), four f32 chains each, from the swizzled A slots
+      float ss[2][4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) ss[t][0] = ss[t][1] = 0ull;
-      auto rms_slot = [&](int t, f32x2 (&acc)[2]) {
+      for (int i = 0; i < 2; ++i) ss[i][0] = ss[i][1] = ss[i][2] = ss[i][3] = 0.0f;
+      auto rms_slot = [&](int t, float (&acc)[4]) {
         if ((t & 1) == wset) {
           const long long s0 = pclk();
           mbar_wait(&a_full[as], aph);
@@ -347,18 +348,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (lane == 0) mbar_arrive(&a_empty[as]);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              f32x2 x;
-              if (kBF16) {
-                x = pack2u(w[e] << 16, w[e] & 0xFFFF0000u);
-              } else {
-                const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
-                x = pack2(f2.x, f2.y);
-              }
-              acc[e & 1] = ffma2(x, x, acc[e & 1]);
-            }
+            sq2_acc<kBF16>(u[j].x, acc[0], acc[1]);
+            sq2_acc<kBF16>(u[j].y, acc[2], acc[3]);
+            sq2_acc<kBF16>(u[j].z, acc[0], acc[1]);
+            sq2_acc<kBF16>(u[j].w, acc[2], acc[3]);
           }
         }
         if (++as == p.na) { as = 0; aph ^= 1; }
@@ -368,13 +361,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int kc = 0; kc < P1; ++kc) {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          if (t < T) rms_slot(t, ss[t]);
+          if (t < T) rms_slot(t, ss[t >> 1]);
       }
       const int par = gi & 1;
       mbar_wait(&m_empty[par], (((uint32_t)gi >> 1) & 1u) ^ 1u);
       // epilogue of one tile: tcgen05.ld the row's b pre-activations, scale,
       // SiLU, dot w_up, f64 sigmoid, strict threshold, ballot -> words
-      auto epilogue = [&](int t, const f32x2 (&acc_ss)[2]) {
+      auto epilogue = [&](int t, const float (&acc_ss)[4]) {
         uint32_t bal = 0;
         if (t < T) {
           mbar_wait(&t_full[t], (accph >> t) & 1u);
@@ -382,10 +375,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (dbg && warp == 2 && lane == 0) dbg[8 + 2 * t] = gtimer();
           const int64_t r = r0 + (int64_t)t * 128 + row;
           const bool valid = r < r1;
-          float sa0, sa1, sb0, sb1;
-          unpack2(acc_ss[0], sa0, sa1);
-          unpack2(acc_ss[1], sb0, sb1);
-          const float sq = (sa0 + sb0) + (sa1 + sb1);
+          const float sq = (acc_ss[0] + acc_ss[1]) + (acc_ss[2] + acc_ss[3]);
           const float scale = rms_scale(sq, p.inv_d, p.eps);
           const float hs = 0.5f * scale;  // exact (power of two)
           const f32x2 hs2 = pack2(hs, hs);
@@ -453,10 +443,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         if (t < T)
-          for (int j = 0; j < p.nx; ++j) rms_slot(t, ss[t]);
+          for (int j = 0; j < p.nx; ++j) rms_slot(t, ss[t >> 1]);
         if ((t & 1) == wset) {
           if (t == wset && dbg && warp == 2 && lane == 0) { dbg[2] = gtimer(); dbg[20] = sw_cyc; dbg[21] = pclk() - s_begin; }
-          epilogue(t, ss[t]);
+          epilogue(t, ss[t >> 1]);
         }
       }
       accph ^= (1u << T) - 1u;

@@ -122,13 +122,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // PDL: inputs written by the previous launch (the peeled chain's live count
+  // and row index) are read only after it completed; otherwise this grid
+  // streams its rows while the previous one finishes its tail, and waits only
+  // before its first global write / look-back (epilogue and compaction warps).
+  const bool dep_inputs = p.n_dev != nullptr || p.row_idx != nullptr;
+  if (dep_inputs) griddep_wait();
+  if (threadIdx.x == 0) griddep_launch_dependents();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
   const int64_t n32 = (n + kGran - 1) / kGran;  // number of kGran-row units
   const int64_t G = gridDim.x;
   const int64_t cpg = (int64_t)p.tpg * (128 / kGran);
   int64_t NG = n32 < G ? n32 : G;
   if ((n32 + cpg - 1) / cpg > NG) NG = (n32 + cpg - 1) / cpg;
-  const uint32_t tag = launch_tag(p.ws);
   const bool gathered = p.row_idx != nullptr;
   const bool need_scan = p.exit_idx || p.cont_idx || p.counts;
   auto bounds = [&](int64_t g, int64_t& r0, int64_t& r1) { group_range(g, n, n32, NG, r0, r1); };
@@ -365,6 +371,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       const int par = gi & 1;
       mbar_wait(&m_empty[par], (((uint32_t)gi >> 1) & 1u) ^ 1u);
+      if (gi == 0) griddep_wait();  // before this grid's first global write
       // epilogue of one tile: tcgen05.ld the row's b pre-activations, scale,
       // SiLU, dot w_up, f64 sigmoid, strict threshold, ballot -> words
       auto epilogue = [&](int t, const float (&acc_ss)[4]) {
@@ -457,6 +464,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
   } else {
     // ----------------------------------------------------------- compaction
+    griddep_wait();  // the previous launch's look-back state / outputs are final
+    const uint32_t tag = launch_tag(p.ws);
     int gi = 0;
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
@@ -713,10 +722,23 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
                          227 * 1024);
     attr_set[dev & 63] = true;
   }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreadsTC);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  {
+    static const char* env = getenv("TIDE_PDL");
+    cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
+  }
+  cfg.attrs = attr;
   if (a.dtype == TIDE_BF16)
-    route_tc_kernel<true><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
+    cudaLaunchKernelEx(&cfg, route_tc_kernel<true>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
   else
-    route_tc_kernel<false><<<grid, kThreadsTC, smem_bytes, stream>>>(tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
+    cudaLaunchKernelEx(&cfg, route_tc_kernel<false>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
   return check_launch("route_tc_kernel");
 }
 

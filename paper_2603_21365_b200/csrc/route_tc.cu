@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int64_t r0, r1;
       bounds(g, r0, r1);
       const int par = gi & 1;
-      mbar_wait_sleep(&m_full[par], ((uint32_t)gi >> 1) & 1u);
+      mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
       __syncwarp();
       if (lane == 0) mbar_arrive(&m_empty[par]);

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(64 + 32 * NR, 1)
         } else {
           mbar_wait(&w_empty[wsl], wph ^ 1);
         }
-        if (p.flags & 4) {
+        if ((p.flags & 4) && !((p.flags & 8) && kc >= p.nw)) {
           mbar_arrive_expect_tx(&w_full[wsl], kSlot);
           tma_load_2d(sW + wsl * kSlot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
         } else {
@@ -300,17 +300,12 @@ int main(int argc, char** argv) {
     p.na = c.na;
     p.nw = c.nw;
     char nm[128];
-    for (uint32_t f : {4u, 5u, 6u, 7u, 3u}) {
+    for (uint32_t f : {7u, 15u, 5u, 13u}) {
       p.flags = f;
-      const char* fs = f == 4 ? "TMA" : f == 5 ? "TMA+MMA" : f == 6 ? "TMA+RMS" : f == 7 ? "TMA+MMA+RMS" : "MMA+RMS(no TMA)";
+      const char* fs = f == 7 ? "TMA+MMA+RMS" : f == 15 ? "TMA+MMA+RMS noW" : f == 5 ? "TMA+MMA" : "TMA+MMA noW";
       snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM0 NR8 RL0 (base)", c.na, c.nw, fs);
       show(nm, run<0, 8, 0>(th, tw, p, sms));
-      snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM1 NR8 (stage)", c.na, c.nw, fs);
-      show(nm, run<1, 8, 0>(th, tw, p, sms));
-      snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM2 NR8 RL0", c.na, c.nw, fs);
-      show(nm, run<2, 8, 0>(th, tw, p, sms));
-      snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM0 NR4 RL0", c.na, c.nw, fs);
-      show(nm, run<0, 4, 0>(th, tw, p, sms));
+
     }
   }
   return 0;

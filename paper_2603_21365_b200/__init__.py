@@ -6,6 +6,9 @@ computed by hand-written sm_100a kernels in `_lib/libtide_b200.so` (C ABI:
 include/tide_b200.h).  No CPU fallback.
 """
 
+from .bank_io import (BadMagicError, BinaryFormatError, ChecksumError, DimensionError,
+                      TruncatedError, VersionError, bank_file_size, install_device_weights,
+                      load_bank, save_bank)
 from .calibration import (CalibrationConfig, CalibrationDataset, CollectedStates, RouterBank,
                           RouterStats, checkpoint_layers, compute_labels, label_tensors,
                           make_bank)
@@ -26,4 +29,6 @@ __all__ = [
     "BATCH_UNANIMOUS", "FINAL_KEY", "MODES", "NO_EXIT", "PER_TOKEN", "OutputHead", "PhaseStats",
     "RuntimeConfig", "posthoc_select", "select_exits",
     "DEFAULT_EPS", "batched_cosine_similarity", "__version__",
+    "load_bank", "save_bank", "bank_file_size", "install_device_weights", "BinaryFormatError",
+    "BadMagicError", "VersionError", "TruncatedError", "ChecksumError", "DimensionError",
 ]

@@ -83,6 +83,13 @@ def device_weights(router, dtype_code: int, device) -> tuple:
     return _weight_cache[key][2], _weight_cache[key][3]
 
 
+def install_cached(router, dtype_code: int, device, wd: torch.Tensor, wu: torch.Tensor) -> None:
+    """Seed the device weight cache with copies made elsewhere (bank_io)."""
+    dev = torch.device(device)
+    _weight_cache[(id(router), dev.index, dtype_code)] = (
+        router.w_down, router.w_up, wd.contiguous(), wu.reshape(-1).contiguous(), router)
+
+
 def _rows_for(h, router):
     """Validate like ee/router_ops.py:53-57; -> (device rows, ld, dtype code, host?)."""
     host = D.is_host(h)

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     const int q = warp & 3;  // TMEM lane quadrant of this warp
     const int row = 32 * q + lane;
     const uint32_t swz = (uint32_t)(row & 7);
-    f32x2 ss0 = 0ull, ss1 = 0ull;
+    float sq[4] = {0.f, 0.f, 0.f, 0.f};
     const int nkr = k1 - k0;
     // Gathered rows (TMA gather4 measured ~2.5x slower than this): cp.async,
     // `stages` chunks ahead.  The warp copies its own 32 rows; one instruction moves 4
@@ -306,26 +306,14 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       if (gathered && i >= 1 && i - 1 + p.stages < nkr) issue(i - 1 + p.stages);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          f32x2 x;
-          if (kBF16) {
-            x = pack2u(w[e] << 16, w[e] & 0xFFFF0000u);
-          } else {
-            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
-            x = pack2(f2.x, f2.y);
-          }
-          if (e & 1) ss1 = ffma2(x, x, ss1);
-          else ss0 = ffma2(x, x, ss0);
-        }
+        sq2_acc<kBF16>(u[j].x, sq[0], sq[1]);
+        sq2_acc<kBF16>(u[j].y, sq[2], sq[3]);
+        sq2_acc<kBF16>(u[j].z, sq[0], sq[1]);
+        sq2_acc<kBF16>(u[j].w, sq[2], sq[3]);
       }
       if (++s == p.stages) { s = 0; ph ^= 1u; }
     }
-    float a0, a1, b0, b1;
-    unpack2(ss0, a0, a1);
-    unpack2(ss1, b0, b1);
-    const float ssp = (a0 + b0) + (a1 + b1);
+    const float ssp = (sq[0] + sq[1]) + (sq[2] + sq[3]);
     for (int i = threadIdx.x - 64; i < p.b; i += 128) sWup[i] = p.w_up[i];  // used after recv_full
     if (warp == 2 && lane == 0) TL(3);
     mbar_wait(acc_full, 0);  // every MMA retired: the stage ring is no longer read by the MMAs
@@ -391,9 +379,8 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     for (int j = 0; j < ks; ++j)
       ss += (j == (int)rank) ? stage_out[(size_t)p.bp * 128 + rank * R + rr] : rss[j * R];
     const float scale = rms_scale(ss, p.inv_d, p.eps);
-    const f32x2 scale2 = pack2(scale, scale);
-    const float nsl = -scale * 1.4426950408889634f;
-    const f32x2 nsl2 = pack2(nsl, nsl);
+    const float hs = 0.5f * scale;  // exact (power of two)
+    const f32x2 hs2 = pack2(hs, hs);
     // 8 columns at a time: 8 independent sums, then 4 independent SiLU pairs
     // (one warp per SMSP here, so ILP is what hides the latency)
     f32x2 acc2 = 0ull, acc2b = 0ull;
@@ -416,7 +403,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         const float w1 = c + 1 < p.b ? sWup[c + 1] : 0.f;
         const float a0 = c < p.b ? sum[u] : 0.f;
         const float a1 = c + 1 < p.b ? sum[u + 1] : 0.f;
-        const f32x2 tt = ffma2(pack2(w0, w1), silu2_fast(pack2(a0, a1), scale2, nsl2), 0ull);
+        const f32x2 tt = ffma2(pack2(w0, w1), silu2_tanh(fmul2(pack2(a0, a1), hs2)), 0ull);
         if (u & 2) acc2b = fadd2(acc2b, tt);
         else acc2 = fadd2(acc2, tt);
       }

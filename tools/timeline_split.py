@@ -1,4 +1,5 @@
-"""Per-CTA timeline of the split-K route kernel (debug).  usage: n d gathered"""
+"""Per-CTA timeline of the split-K route kernel (debug).
+usage: n d gathered [live]   (live: row count in device memory, n = capacity)"""
 import ctypes
 import os
 import sys
@@ -12,6 +13,8 @@ from paper_2603_21365_b200 import _device as D, _native as N  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 gathered = len(sys.argv) > 3 and sys.argv[3] == "1"
+live = int(sys.argv[4]) if len(sys.argv) > 4 else None
+n_dev = torch.tensor([live], dtype=torch.int64, device="cuda") if live is not None else None
 b = 128
 rows = 2 * n if gathered else n
 h = torch.randn((rows, d), device="cuda").to(torch.bfloat16)
@@ -28,7 +31,7 @@ ws = D.workspace().data_ptr()
 
 
 def launch():
-    N.check(lib.tide_route(h.data_ptr(), d, n, None, rows, d, N.BF16,
+    N.check(lib.tide_route(h.data_ptr(), d, n, n_dev.data_ptr() if live is not None else None, rows, d, N.BF16,
                            idx.data_ptr() if gathered else None, wd.data_ptr(), wu.data_ptr(), b,
                            1e-6, 0.5, 3, None, logits.data_ptr(), None, None, cont.data_ptr(), 1,
                            None, counts.data_ptr(), ws, D.stream_handle()), "route")
@@ -42,7 +45,7 @@ for it in range(5):
     e.record()
     torch.cuda.synchronize()
 lib.tide_debug_timeline(None)
-print(f"n={n} d={d} gathered={gathered}: event time of the traced launch {a.elapsed_time(e) * 1e3:.1f} us")
+print(f"n={n} live={live} d={d} gathered={gathered}: event time of the traced launch {a.elapsed_time(e) * 1e3:.1f} us")
 t = dbg.view(148, 24).cpu().numpy().astype(np.int64)
 live = t[:, 0] > 0
 t = t[live]

@@ -19,6 +19,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -67,10 +70,84 @@ __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, boo
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
 
 template <typename T>
 __device__ __forceinline__ void lds_vec(const T* p, float (&f)[16 / sizeof(T)]) {
   unpack16(*reinterpret_cast<const uint4*>(p), f, (const T*)nullptr);
+}
+
+// Step 5 (+ the exit resolution), shared: one CTA per checkpoint holds the
+// row logits in sLogit[NR]; scores out, then the last checkpoint to finish
+// (atomic ticket) resolves per-token / batch-unanimous exits.
+template <int NR>
+__device__ __forceinline__ void decode_finish(const DecParams& p, int c, const float* sLogit,
+                                              unsigned int* last_s, bool reset_ticket = true) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = (int)p.n;
+  if (threadIdx.x < NR && threadIdx.x < n) {
+    const int r = threadIdx.x;
+    const float t = sLogit[r];
+    const float score = score_from_logit(t);
+    if (p.scores) p.scores[(int64_t)c * n + r] = score;
+    if (p.logits) p.logits[(int64_t)c * n + r] = t;
+    p.ws->dec_scores[c * kDMaxRows + r] = score;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (reset_ticket) p.ws->tickets[c] = 0;  // reset for the next launch (graph replay safe)
+    const unsigned int prev = atomicAdd(&p.ws->ticket, 1u);
+    *last_s = (prev == (unsigned int)(p.C - 1)) ? 2u : 0u;
+  }
+  __syncthreads();
+  DTL(5);
+  if (*last_s != 2u || warp != 0) return;
+  __threadfence();
+  // exit resolution: lanes = rows; scores of 8 checkpoints in flight at once
+  const int r = lane;
+  int64_t exit_layer = TIDE_NO_EXIT;
+  bool done = false;
+  for (int cb = 0; cb < p.C && !done; cb += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = (cb + u < p.C && r < n) ? __ldcg(&p.ws->dec_scores[(cb + u) * kDMaxRows + r]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int cc = cb + u;
+      if (done || cc >= p.C || p.layers[cc] < p.k_min) continue;
+      if (p.mode == TIDE_MODE_PER_TOKEN) {
+        if (r < n && exit_layer == TIDE_NO_EXIT && v[u] > p.theta) exit_layer = p.layers[cc];
+        done = __all_sync(0xffffffffu, r >= n || exit_layer != TIDE_NO_EXIT);
+      } else if (__all_sync(0xffffffffu, r >= n || v[u] > p.theta)) {
+        exit_layer = p.layers[cc];
+        done = true;
+      }
+    }
+  }
+  if (r < n && p.exit_layers) p.exit_layers[r] = exit_layer;
+  const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, r < n && exit_layer != TIDE_NO_EXIT));
+  if (lane == 0) {
+    if (p.exit_count) p.exit_count[0] = cnt;
+    p.ws->ticket = 0;
+  }
+  DTL(6);
 }
 
 // Steps 3-4, shared by both kernels.  sRes [b][NR] + sSS [NR] hold this CTA's
@@ -141,55 +218,13 @@ __device__ __forceinline__ void decode_tail(const DecParams& p, int c, int s, fl
     if (lane < NR) sLog[warp * NR + lane] = t;
   }
   __syncthreads();
-  if (threadIdx.x < NR && threadIdx.x < n) {
-    const int r = threadIdx.x;
+  if (threadIdx.x < NR) {
     float t = 0.f;
-    for (int w = 0; w < kDWarps; ++w) t += sLog[w * NR + r];
-    const float score = score_from_logit(t);
-    if (p.scores) p.scores[(int64_t)c * n + r] = score;
-    if (p.logits) p.logits[(int64_t)c * n + r] = t;
-    p.ws->dec_scores[c * kDMaxRows + r] = score;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    p.ws->tickets[c] = 0;  // reset for the next launch (graph replay safe)
-    const unsigned int prev = atomicAdd(&p.ws->ticket, 1u);
-    *last_s = (prev == (unsigned int)(p.C - 1)) ? 2u : 0u;
+    for (int w = 0; w < kDWarps; ++w) t += sLog[w * NR + threadIdx.x];
+    sLog[kDWarps * NR + threadIdx.x] = t;
   }
   __syncthreads();
-  DTL(5);
-  if (*last_s != 2u || warp != 0) return;
-  __threadfence();
-  // exit resolution: lanes = rows; scores of 8 checkpoints in flight at once
-  const int r = lane;
-  int64_t exit_layer = TIDE_NO_EXIT;
-  bool done = false;
-  for (int cb = 0; cb < p.C && !done; cb += 8) {
-    float v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      v[u] = (cb + u < p.C && r < n) ? __ldcg(&p.ws->dec_scores[(cb + u) * kDMaxRows + r]) : 0.f;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int cc = cb + u;
-      if (done || cc >= p.C || p.layers[cc] < p.k_min) continue;
-      if (p.mode == TIDE_MODE_PER_TOKEN) {
-        if (r < n && exit_layer == TIDE_NO_EXIT && v[u] > p.theta) exit_layer = p.layers[cc];
-        done = __all_sync(0xffffffffu, r >= n || exit_layer != TIDE_NO_EXIT);
-      } else if (__all_sync(0xffffffffu, r >= n || v[u] > p.theta)) {
-        exit_layer = p.layers[cc];
-        done = true;
-      }
-    }
-  }
-  if (r < n && p.exit_layers) p.exit_layers[r] = exit_layer;
-  const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, r < n && exit_layer != TIDE_NO_EXIT));
-  if (lane == 0) {
-    if (p.exit_count) p.exit_count[0] = cnt;
-    p.ws->ticket = 0;
-  }
-  DTL(6);
+  decode_finish<NR>(p, c, sLog + kDWarps * NR, last_s);
 }
 
 // ---------------------------------------------------------------------------
@@ -198,7 +233,10 @@ __device__ __forceinline__ void decode_tail(const DecParams& p, int c, int s, fl
 //   sB [nkc][16 rows x 128 B]       hidden rows (zero past n), SW128 K-major
 //   then sRes [b][NR] + sSS [NR], sLog [8][NR], sWup [b], barrier, TMEM slot
 // ---------------------------------------------------------------------------
-template <bool kBF16, int NR>
+// kClu: the S slice-CTAs of a checkpoint form one thread-block cluster and
+// reduce their partial tiles through distributed shared memory (two cluster
+// barriers) instead of partials -> workspace -> ticket -> last-CTA re-read.
+template <bool kBF16, int NR, bool kClu>
 __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_constant__ DecParams p) {
   using T = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
   constexpr int V = 8;
@@ -215,10 +253,11 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   uint8_t* sB = sA + (size_t)nkc * MT * 16384;
   float* sRes = reinterpret_cast<float*>(sB + (size_t)nkc * 2048);
   float* sLog = sRes + (size_t)b * NR + NR;
-  float* sWup = sLog + kDWarps * NR;
+  float* sWup = sLog + (kDWarps + 1) * NR;
   uint64_t* mma_done = reinterpret_cast<uint64_t*>(sWup + ((b + 1) & ~1));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 1);
   DTL(0);
+  if (kClu) cluster_arrive_relaxed();  // this CTA's smem exists (peers write it after step 3a)
 
   // 1. one round trip: W slice + hidden slice as 16-byte pieces into the
   //    swizzled K-major layout (piece q of row j at ((q ^ (j & 7)) << 4))
@@ -313,7 +352,61 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
     tmem_dealloc(tmem_base, 32);
   }
   DTL(2);
-  decode_tail<NR>(p, c, s, sRes, sWup, sLog, &last_s);
+  if (!kClu) {
+    decode_tail<NR>(p, c, s, sRes, sWup, sLog, &last_s);
+    return;
+  }
+  // 3b. DSMEM reduction.  Rank q owns units [q U, (q+1) U); every CTA stores its
+  // partial of those units into q's recv[src = own rank], and its partial sum
+  // of squares into every CTA's recv_ss[src].
+  const uint32_t rank = (uint32_t)s;  // cluster dims (S, 1, 1), blockIdx.x = c S + s
+  const int S = p.S, U = (b + S - 1) / S;
+  float* recv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
+  float* recv_ss = recv + (size_t)S * U * NR;
+  float* plog = recv_ss + (size_t)S * NR;
+  float* yv = plog + (size_t)S * NR;
+  const float* sSS = sRes + (size_t)b * NR;
+  cluster_wait();  // every peer started
+  for (int i = threadIdx.x; i < b * NR; i += kDThreads) {
+    const int j = i / NR, r = i - j * NR;
+    const int q = j / U, uu = j - q * U;
+    st_dsmem_f32(dsmem_addr(smem_u32(recv + ((size_t)rank * U + uu) * NR + r), (uint32_t)q), sRes[i]);
+  }
+  for (int i = threadIdx.x; i < S * NR; i += kDThreads) {
+    const int q = i / NR, r = i - q * NR;
+    st_dsmem_f32(dsmem_addr(smem_u32(recv_ss + rank * NR + r), (uint32_t)q), sSS[r]);
+  }
+  cluster_sync_all();  // release / acquire: every partial landed
+  DTL(3);
+  // 4. this CTA's units: totals over the S slices (fixed order), scale,
+  //    SiLU, w_up; partial logit per row -> rank 0's plog[rank]
+  for (int i = threadIdx.x; i < U * NR; i += kDThreads) {
+    const int uu = i / NR, r = i - uu * NR;
+    const int j = (int)rank * U + uu;
+    float a = 0.f, ss = 0.f;
+    for (int src = 0; src < S; ++src) {
+      a += recv[((size_t)src * U + uu) * NR + r];
+      ss += recv_ss[src * NR + r];
+    }
+    const float scale = rms_scale(ss, p.inv_d, p.eps);
+    yv[i] = j < b ? __fmul_rn(sWup[j], silu_f32(__fmul_rn(a, scale))) : 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x < NR) {
+    float t = 0.f;
+    for (int uu = 0; uu < U; ++uu) t += yv[uu * NR + threadIdx.x];
+    st_dsmem_f32(dsmem_addr(smem_u32(plog + rank * NR + threadIdx.x), 0u), t);
+  }
+  cluster_sync_all();  // rank 0 holds every partial logit; no DSMEM traffic after this
+  DTL(4);
+  if (rank != 0) return;
+  if (threadIdx.x < NR) {
+    float t = 0.f;
+    for (int src = 0; src < S; ++src) t += plog[src * NR + threadIdx.x];
+    yv[threadIdx.x] = t;
+  }
+  __syncthreads();
+  decode_finish<NR>(p, c, yv, &last_s, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -335,7 +428,7 @@ __global__ void __launch_bounds__(kDThreads) decode_f32_kernel(const __grid_cons
   T* sH = sW + (size_t)b * p.cs;             // [NR][cs]
   float* sRes = sH + (size_t)NR * p.cs;      // [b][NR] + [NR]
   float* sLog = sRes + (size_t)b * NR + NR;  // [8][NR]
-  float* sWup = sLog + kDWarps * NR;         // [b]
+  float* sWup = sLog + (kDWarps + 1) * NR;   // [b]
   DTL(0);
   const T* W = reinterpret_cast<const T*>(p.w[c]);
   const T* H = reinterpret_cast<const T*>(p.h[c]);
@@ -414,13 +507,82 @@ __global__ void __launch_bounds__(kDThreads) decode_f32_kernel(const __grid_cons
   decode_tail<NR>(p, c, s, sRes, sWup, sLog, &last_s);
 }
 
-size_t tail_bytes(int b, int NR) { return ((size_t)b * NR + NR + kDWarps * NR + b + 2) * 4; }
+size_t tail_bytes(int b, int NR) { return ((size_t)b * NR + NR + (kDWarps + 1) * NR + b + 2) * 4; }
 
 size_t smem_tc(int b, int cs, int NR) {
   const int MT = (b + 127) / 128, nkc = cs / 64;
   return 1024 + (size_t)nkc * MT * 16384 + (size_t)nkc * 2048 + tail_bytes(b, NR) + 32;
 }
+// extra smem of the cluster variant: recv [S][U][NR] + recv_ss [S][NR] + plog [S][NR] + yv [U][NR]
+size_t smem_clu(int b, int S, int NR) {
+  const int U = (b + S - 1) / S;
+  return 16 + ((size_t)S * U * NR + 2 * (size_t)S * NR + (size_t)U * NR) * 4;
+}
 size_t smem_f32(int b, int cs, int NR) { return (size_t)(b + NR) * cs * 4 + tail_bytes(b, NR); }
+
+// Largest-cluster plan: clusters of S slice-CTAs (one per checkpoint) when all
+// C of them can be co-resident; else 0 (the global-ticket reduction).
+template <typename K>
+int launch_cluster(K kernel, const DecParams& p, size_t smem, cudaStream_t s) {
+  // co-resident cluster counts per (kernel, S, smem), queried once each
+  struct Entry {
+    const void* k;
+    size_t smem;
+    int S, v;
+  };
+  static Entry cache[16];
+  static int used = 0;
+  static std::mutex mu;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.C * p.S));
+  cfg.blockDim = dim3(kDThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = (unsigned)p.S;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  int ok_for = -1;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < used; ++i)
+      if (cache[i].k == (const void*)kernel && cache[i].smem == smem && cache[i].S == p.S) ok_for = cache[i].v;
+    if (ok_for < 0) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      int v = 0;
+      if (cudaOccupancyMaxActiveClusters(&v, kernel, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        v = 0;
+      }
+      ok_for = v;
+      if (used < 16) cache[used++] = Entry{(const void*)kernel, smem, p.S, v};
+      if (getenv("TIDE_DEBUG_PLAN"))
+        fprintf(stderr, "[tide] decode clusters of %d x %zu B smem: %d co-resident (need %d)\n",
+                p.S, smem, v, p.C);
+    }
+  }
+  {
+    // the dynamic-smem attribute is per kernel: keep it at the largest size launched
+    static const void* ks[8];
+    static size_t kmax[8];
+    static int nk = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    int i = 0;
+    while (i < nk && ks[i] != (const void*)kernel) ++i;
+    if (i == nk && nk < 8) { ks[nk] = (const void*)kernel; kmax[nk++] = 0; }
+    if (i < 8 && kmax[i] < smem) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kmax[i] = smem;
+    }
+  }
+  if (ok_for < p.C) return 1;  // not co-resident: caller falls back
+  cudaLaunchKernelEx(&cfg, kernel, p);
+  return check_launch("decode_tc_kernel (cluster)") == TIDE_OK ? 0 : -1;
+}
 
 template <typename K>
 int launch_kernel(K kernel, const DecParams& p, size_t smem, cudaStream_t s, size_t* attr) {
@@ -499,12 +661,34 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
   p.dbg = g_dbg;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   static size_t attr[6] = {0, 0, 0, 0, 0, 0};
+  // tensor-core path: slice CTAs of a checkpoint as one cluster (DSMEM
+  // reduction) when S <= 16 and all C clusters fit; TIDE_DECODE_CLUSTER=0 disables
+  static const char* cenv = getenv("TIDE_DECODE_CLUSTER");
+  if (tc && !(cenv && cenv[0] == '0')) {
+    // widest slice first (S = 16, then 8): fewer bytes per CTA, if co-resident
+    for (int cw = cs; cw <= 4 * cs; cw *= 2) {
+      DecParams q = p;
+      q.cs = cw;
+      q.S = (d + cw - 1) / cw;
+      if (q.S < 2 || q.S > 16 || q.cs % 64) continue;
+      const size_t smc = smem_tc(b, cw, NR) + smem_clu(b, q.S, NR);
+      if (smc > 220 * 1024) break;
+      int rc;
+      if (dtype == TIDE_BF16)
+        rc = NR == 8 ? launch_cluster(decode_tc_kernel<true, 8, true>, q, smc, s)
+                     : launch_cluster(decode_tc_kernel<true, 16, true>, q, smc, s);
+      else
+        rc = NR == 8 ? launch_cluster(decode_tc_kernel<false, 8, true>, q, smc, s)
+                     : launch_cluster(decode_tc_kernel<false, 16, true>, q, smc, s);
+      if (rc <= 0) return rc == 0 ? TIDE_OK : TIDE_ERR_CUDA;
+    }
+  }
   if (dtype == TIDE_BF16)
-    return NR == 8 ? launch_kernel(decode_tc_kernel<true, 8>, p, smem, s, &attr[0])
-                   : launch_kernel(decode_tc_kernel<true, 16>, p, smem, s, &attr[1]);
+    return NR == 8 ? launch_kernel(decode_tc_kernel<true, 8, false>, p, smem, s, &attr[0])
+                   : launch_kernel(decode_tc_kernel<true, 16, false>, p, smem, s, &attr[1]);
   if (dtype == TIDE_F16)
-    return NR == 8 ? launch_kernel(decode_tc_kernel<false, 8>, p, smem, s, &attr[2])
-                   : launch_kernel(decode_tc_kernel<false, 16>, p, smem, s, &attr[3]);
+    return NR == 8 ? launch_kernel(decode_tc_kernel<false, 8, false>, p, smem, s, &attr[2])
+                   : launch_kernel(decode_tc_kernel<false, 16, false>, p, smem, s, &attr[3]);
   return NR == 8 ? launch_kernel(decode_f32_kernel<8>, p, smem, s, &attr[4])
                  : launch_kernel(decode_f32_kernel<16>, p, smem, s, &attr[5]);
 }

@@ -37,7 +37,14 @@ constexpr int kDMaxRows = TIDE_MAX_DECODE_ROWS;
 constexpr int kDMaxC = kMaxTickets;
 constexpr int kDMaxB = 256;
 
+constexpr int kDMaxKc = 16;  // 64-column k-chunks per slice (TMA path)
+
 struct DecParams {
+  // W of every checkpoint stacked as [C * b, d] (the runtime's decode plan):
+  // one tensor map, one TMA box (64 columns x 128 rows) per k-chunk and
+  // 128-row block; use_tma = 0 falls back to per-thread cp.async
+  CUtensorMap wmap;
+  int32_t use_tma;
   const void* h[kDMaxC];
   const void* w[kDMaxC];
   const float* wup[kDMaxC];
@@ -264,12 +271,29 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   const T* W = reinterpret_cast<const T*>(p.w[c]);
   const T* H = reinterpret_cast<const T*>(p.h[c]);
   const int per_row = nkc * 8;
-  for (int i = threadIdx.x; i < b * per_row; i += kDThreads) {
-    const int j = i / per_row, rem = i - j * per_row, kc = rem >> 3, q = rem & 7;
-    const int col = c0 + kc * 64 + q * 8;
-    const bool in = col < p.d;
-    uint8_t* dst = sA + ((size_t)kc * MT + (j >> 7)) * 16384 + (j & 127) * 128 + ((q ^ (j & 7)) << 4);
-    cp_async16_zfill(dst, W + (int64_t)j * p.d + (in ? col : 0), in);
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tmem_slot) + 8);  // [kDMaxKc]
+  if (p.use_tma) {
+    // W slice by TMA, one barrier per k-chunk: the MMAs of early chunks run
+    // while later chunks land
+    if (threadIdx.x == 0) {
+      for (int kc = 0; kc < nkc; ++kc) mbar_init(&wfull[kc], 1);
+      fence_mbar_init();
+      const uint64_t pol = policy_evict_last();  // every decode step re-reads it
+      for (int kc = 0; kc < nkc; ++kc) {
+        mbar_arrive_expect_tx(&wfull[kc], (uint32_t)MT * 16384u);
+        for (int mt = 0; mt < MT; ++mt)
+          tma_load_2d(sA + ((size_t)kc * MT + mt) * 16384, &p.wmap, &wfull[kc], c0 + kc * 64,
+                      c * b + mt * 128, pol);
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < b * per_row; i += kDThreads) {
+      const int j = i / per_row, rem = i - j * per_row, kc = rem >> 3, q = rem & 7;
+      const int col = c0 + kc * 64 + q * 8;
+      const bool in = col < p.d;
+      uint8_t* dst = sA + ((size_t)kc * MT + (j >> 7)) * 16384 + (j & 127) * 128 + ((q ^ (j & 7)) << 4);
+      cp_async16_zfill(dst, W + (int64_t)j * p.d + (in ? col : 0), in);
+    }
   }
   for (int i = threadIdx.x; i < 16 * per_row; i += kDThreads) {
     const int r = i / per_row, rem = i - r * per_row, kc = rem >> 3, q = rem & 7;
@@ -301,8 +325,12 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
     if (elect_one()) {
       const uint64_t desc_hi = sw128_kmajor_desc(0);
       const uint32_t idesc = f16_idesc(kBF16 ? 1 : 0, 128, 16);
-      for (int mt = 0; mt < MT; ++mt)
-        for (int kc = 0; kc < nkc; ++kc) {
+      for (int kc = 0; kc < nkc; ++kc) {
+        if (p.use_tma) {
+          mbar_wait(&wfull[kc], 0);
+          tc_fence_after();
+        }
+        for (int mt = 0; mt < MT; ++mt) {
           const uint64_t ad =
               desc_hi | (uint64_t)((smem_u32(sA + ((size_t)kc * MT + mt) * 16384) & 0x3FFFFu) >> 4);
           const uint64_t bd = desc_hi | (uint64_t)((smem_u32(sB + (size_t)kc * 2048) & 0x3FFFFu) >> 4);
@@ -310,6 +338,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
           for (int k = 0; k < 4; ++k)
             tc_mma_f16(tmem_base + (uint32_t)(mt * 16), ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
         }
+      }
       tc_commit(mma_done);
     }
     __syncwarp();
@@ -361,7 +390,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   // of squares into every CTA's recv_ss[src].
   const uint32_t rank = (uint32_t)s;  // cluster dims (S, 1, 1), blockIdx.x = c S + s
   const int S = p.S, U = (b + S - 1) / S;
-  float* recv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
+  float* recv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 8 + 8 * kDMaxKc);
   float* recv_ss = recv + (size_t)S * U * NR;
   float* plog = recv_ss + (size_t)S * NR;
   float* yv = plog + (size_t)S * NR;
@@ -511,7 +540,7 @@ size_t tail_bytes(int b, int NR) { return ((size_t)b * NR + NR + (kDWarps + 1) *
 
 size_t smem_tc(int b, int cs, int NR) {
   const int MT = (b + 127) / 128, nkc = cs / 64;
-  return 1024 + (size_t)nkc * MT * 16384 + (size_t)nkc * 2048 + tail_bytes(b, NR) + 32;
+  return 1024 + (size_t)nkc * MT * 16384 + (size_t)nkc * 2048 + tail_bytes(b, NR) + 32 + 8 * kDMaxKc;
 }
 // extra smem of the cluster variant: recv [S][U][NR] + recv_ss [S][NR] + plog [S][NR] + yv [U][NR]
 size_t smem_clu(int b, int S, int NR) {
@@ -659,6 +688,19 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
   p.exit_count = exit_count;
   p.ws = reinterpret_cast<Workspace*>(workspace);
   p.dbg = g_dbg;
+  // stacked W ([C, b, d] contiguous, the runtime's decode plan) -> one tensor map
+  p.use_tma = 0;
+  if (tc && d % 8 == 0 && cs / 64 <= kDMaxKc) {
+    bool stacked = true;
+    const char* w0 = reinterpret_cast<const char*>(w_ptrs[0]);
+    for (int c = 1; c < C && stacked; ++c)
+      stacked = reinterpret_cast<const char*>(w_ptrs[c]) == w0 + (size_t)c * b * d * 2;
+    static const char* tenv = getenv("TIDE_DECODE_TMA");
+    if (stacked && !(tenv && tenv[0] == '0') &&
+        make_map(&p.wmap, w_ptrs[0], dtype, d, (int64_t)C * b, d, 64, 128) == TIDE_OK)
+      p.use_tma = 1;
+    cudaGetLastError();
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   static size_t attr[6] = {0, 0, 0, 0, 0, 0};
   // tensor-core path: slice CTAs of a checkpoint as one cluster (DSMEM

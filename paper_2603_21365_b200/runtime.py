@@ -189,9 +189,14 @@ def _decode_plan(bank, ckpts, code, dev):
                                for r, (h, wd, wu) in zip(routers, hit[0])):
         return hit[1]
     ws_w = [device_weights(r, code, dev) for r in routers]
-    arrays = (N.ptr_array([w.data_ptr() for w, _ in ws_w]),
+    # W of all checkpoints stacked [C, b, d]: the decode kernel then loads its
+    # slices with one TMA tensor map (tide_route_decode detects the layout)
+    stacked = torch.stack([w for w, _ in ws_w]).contiguous()
+    step = stacked[0].numel() * stacked.element_size()
+    base = stacked.data_ptr()
+    arrays = (N.ptr_array([base + i * step for i in range(len(routers))]),
               N.ptr_array([u.data_ptr() for _, u in ws_w]), N.i64_array(ckpts))
-    _decode_plans[key] = ([(r, r.w_down, r.w_up) for r in routers], arrays, ws_w, bank)
+    _decode_plans[key] = ([(r, r.w_down, r.w_up) for r in routers], arrays, (ws_w, stacked), bank)
     return arrays
 
 

@@ -121,6 +121,36 @@ __global__ void __launch_bounds__(64 + 32 * NR, 1)
     for (int kc = 0; kc < p.nk; ++kc) {
       mbar_wait(&w_full[wsl], wph);
       const uint64_t bdesc = dhi | (uint64_t)((smem_u32(sW + wsl * kSlot) & 0x3FFFFu) >> 4);
+      if (p.flags & 16) {
+        // k-step-outer: all T slots of the chunk, then W slice k for every tile
+        // pairs of tiles: W slice k feeds two tiles back to back
+        for (int t0 = 0; t0 < T; t0 += 2) {
+          const int np = (T - t0) < 2 ? 1 : 2;
+          int sl[2];
+          for (int u = 0; u < np; ++u) {
+            sl[u] = as;
+            mbar_wait(&a_full[as], aph);
+            if (++as == p.na) { as = 0; aph ^= 1; }
+          }
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+                if (u < np) {
+                  const uint64_t adesc = dhi | (uint64_t)((smem_u32(sA + sl[u] * kSlot) & 0x3FFFFu) >> 4);
+                  tc_mma_f16(tmem + (t0 + u) * 128, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+                }
+            for (int u = 0; u < np; ++u) tc_commit(&a_empty[sl[u]]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) tc_commit(&w_empty[wsl]);
+        __syncwarp();
+        if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
+        continue;
+      }
       for (int t = 0; t < T; ++t) {
         mbar_wait(&a_full[as], aph);
         tc_fence_after();
@@ -300,9 +330,9 @@ int main(int argc, char** argv) {
     p.na = c.na;
     p.nw = c.nw;
     char nm[128];
-    for (uint32_t f : {7u, 15u, 5u, 13u}) {
+    for (uint32_t f : {7u, 23u, 5u, 21u}) {
       p.flags = f;
-      const char* fs = f == 7 ? "TMA+MMA+RMS" : f == 15 ? "TMA+MMA+RMS noW" : f == 5 ? "TMA+MMA" : "TMA+MMA noW";
+      const char* fs = f == 7 ? "TMA+MMA+RMS" : f == 23 ? "TMA+MMA+RMS kpair" : f == 5 ? "TMA+MMA" : "TMA+MMA kpair";
       snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM0 NR8 RL0 (base)", c.na, c.nw, fs);
       show(nm, run<0, 8, 0>(th, tw, p, sms));
 

@@ -30,7 +30,7 @@ constexpr int kGranS = 16;
 struct SkelParams {
   int n, d, nk, na, nw;
   uint32_t flags;  // 1 = MMA, 2 = RMS reads, 4 = TMA
-  uint32_t idesc;
+  uint32_t idesc, idesc2, idesc64;
   float* out;
 };
 
@@ -121,6 +121,31 @@ __global__ void __launch_bounds__(64 + 32 * NR, 1)
     for (int kc = 0; kc < p.nk; ++kc) {
       mbar_wait(&w_full[wsl], wph);
       const uint64_t bdesc = dhi | (uint64_t)((smem_u32(sW + wsl * kSlot) & 0x3FFFFu) >> 4);
+      if (p.flags & 32) {
+        // transposed: D^T[b, 256 tokens] = W (A, M=128) x tokens (B, N=256) over
+        // two adjacent 128-row slots; one MMA per k-step covers two tiles
+        for (int t0 = 0; t0 < T; t0 += 2) {
+          int sl0 = as;
+          for (int u = 0; u < 2; ++u) {
+            mbar_wait(&a_full[as], aph);
+            if (++as == p.na) { as = 0; aph ^= 1; }
+          }
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t tdesc = dhi | (uint64_t)((smem_u32(sA + sl0 * kSlot) & 0x3FFFFu) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(tmem + (t0 >> 1) * 256, bdesc + 2 * k, tdesc + 2 * k, p.idesc2, (kc | k) != 0);
+            tc_commit(&a_empty[sl0]);
+            tc_commit(&a_empty[sl0 + 1]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) tc_commit(&w_empty[wsl]);
+        __syncwarp();
+        if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
+        continue;
+      }
       if (p.flags & 16) {
         // k-step-outer: all T slots of the chunk, then W slice k for every tile
         // pairs of tiles: W slice k feeds two tiles back to back
@@ -156,10 +181,12 @@ __global__ void __launch_bounds__(64 + 32 * NR, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint64_t adesc = dhi | (uint64_t)((smem_u32(sA + as * kSlot) & 0x3FFFFu) >> 4);
-          if (p.flags & 1)
+          if (p.flags & 1) {
+            const uint32_t id = ((p.flags & 64) && t == T - 1) ? p.idesc64 : p.idesc;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              tc_mma_f16(tmem + t * 128, adesc + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+              tc_mma_f16(tmem + t * 128, adesc + 2 * k, bdesc + 2 * k, id, (kc | k) != 0);
+          }
           if (CM == 0 || CM == 2) tc_commit(&a_empty[as]);
           if (CM == 2 && t == T - 1) tc_commit(&w_empty[wsl]);
         }
@@ -320,19 +347,20 @@ int main(int argc, char** argv) {
   CUtensorMap th = make(h, d, n, 64, 128), tw = make(w, d, b, 64, 128);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  SkelParams p{n, d, d / 64, 9, 4, 7u, f16_idesc(1, 128, 128), out};
+  SkelParams p{n, d, d / 64, 9, 4, 7u, f16_idesc(1, 128, 128), f16_idesc(1, 128, 256), f16_idesc(1, 64, 128), out};
   const double bytes = (double)n * d * 2;
   auto show = [&](const char* name, float us) {
     printf("%-58s %8.1f us  %6.0f GB/s\n", name, us, bytes / us / 1e3);
   };
   struct Cfg { int na, nw; };
-  for (Cfg c : {Cfg{9, 4}}) {
+  for (Cfg c : {Cfg{9, 4}, Cfg{8, 4}}) {
     p.na = c.na;
     p.nw = c.nw;
     char nm[128];
-    for (uint32_t f : {7u, 23u, 5u, 21u}) {
+    for (uint32_t f : {7u, 71u, 39u}) {
+      if ((f & 32) && c.na % 2) continue;
       p.flags = f;
-      const char* fs = f == 7 ? "TMA+MMA+RMS" : f == 23 ? "TMA+MMA+RMS kpair" : f == 5 ? "TMA+MMA" : "TMA+MMA kpair";
+      const char* fs = f == 7 ? "TMA+MMA+RMS" : f == 71 ? "TMA+MMA+RMS lastM64" : "TMA+MMA+RMS N256";
       snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM0 NR8 RL0 (base)", c.na, c.nw, fs);
       show(nm, run<0, 8, 0>(th, tw, p, sms));
 

@@ -156,6 +156,28 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   // groups of ks CTAs, one 128-row tile per group, ks chosen HERE from the live
   // row count (n may come from device memory: later links of a peeling chain
   // split their few remaining tiles further).
+  // PDL: the next launch may be scheduled as this grid's CTAs exit.  Setup
+  // that touches no global memory (barriers, TMEM, tensor-map prefetch) runs
+  // before griddepcontrol.wait, so it overlaps the previous link's tail; the
+  // live count and row index it wrote are read after.
+  if (threadIdx.x == 0) griddep_launch_dependents();
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_w);
+    if (p.row_idx == nullptr) prefetch_tmap(&tm_h);
+    for (int i = 0; i < p.stages; ++i) {
+      // gathered: + one cp.async arrive per RMS thread (they copy the rows)
+      mbar_init(&full[i], p.row_idx != nullptr ? 1 + 128 : 1);
+      mbar_init(&empty[i], 1 + 4);  // MMA commit + the 4 RMS warps
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(recv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, p.tmem_cols);
+    tmem_relinquish();
+  }
+  griddep_wait();
   const uint32_t crank = cluster_rank();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
   const int64_t ntiles = (n + 127) / 128;
@@ -175,7 +197,12 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     cluster_wait();
     cluster_arrive_relaxed();
     cluster_wait();
+    tc_fence_before();
     __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc(*tmem_slot, p.tmem_cols);
+    }
     if (threadIdx.x == 0) launch_done(p.ws);
     return;
   }
@@ -185,23 +212,9 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   const bool gathered = p.row_idx != nullptr;
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tm_w);
-    if (!gathered) prefetch_tmap(&tm_h);
-    for (int i = 0; i < p.stages; ++i) {
-      // gathered: + one cp.async arrive per RMS thread (they copy the rows)
-      mbar_init(&full[i], gathered ? 1 + 128 : 1);
-      mbar_init(&empty[i], 1 + 4);  // MMA commit + the 4 RMS warps
-    }
-    mbar_init(acc_full, 1);
-    mbar_init(recv_full, 1);
     // ks - 1 bulk copies of [bp + 1][128 / ks] floats land here (complete_tx may
     // precede this expect_tx: the phase needs the arrive as well)
     mbar_arrive_expect_tx(recv_full, (uint32_t)(ks - 1) * (uint32_t)(p.bp + 1) * (512u / ks));
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(tmem_slot, p.tmem_cols);
-    tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
@@ -653,13 +666,18 @@ int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) 
   cfg.blockDim = dim3(kThreadsS, 1, 1);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)ks;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  {
+    static const char* env = getenv("TIDE_PDL");
+    cfg.numAttrs = (env && env[0] == '0') ? 1 : 2;
+  }
   cudaError_t e;
   if (a.dtype == TIDE_BF16)
     e = cudaLaunchKernelEx(&cfg, route_tcs_kernel<true>, tm_h, tm_w, p);

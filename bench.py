@@ -60,8 +60,9 @@ class ClockSampler:
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 100):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
         self.lines = []
         self.thread = None
@@ -70,7 +71,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (FileNotFoundError, OSError):
             self.proc = None
@@ -267,20 +268,12 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    # parity spot-check of the warm state on rank 0 (first 2,048 rows vs the oracle)
-    if rank == 0 and not args.no_check:
-        hs = h[:2048].float().cpu().numpy()
-        _, t_ref, m_ref = O.route_logits(hs, orouter)
-        ok = O.decision_band_ok(mask[:2048].cpu().numpy(), t_ref, m_ref, THETA, 2e-2)
-        assert ok.all(), "bench parity spot-check failed"
-        e_ref, _ = O.compact_indices(mask.cpu().numpy())
-        assert np.array_equal(exit_idx[: int(counts[0])].cpu().numpy(), e_ref)
-
+    # the clock sampler starts first so the warm-up launches run right before
+    # the timed region (no idle gap for the clocks to drop in)
     clocks = ClockSampler(local)
     clocks.start()
+    for _ in range(args.warmup):
+        step()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -295,6 +288,25 @@ def run_ours(args):
     gpu_launches = launches["n"]
     clk = clocks.stop()
     ms_total = t0.elapsed_time(t1)
+    # The timed region is a few ms, shorter than nvidia-smi's sampling period:
+    # also sample a sustained window of the same step back to back (~0.6 s) so
+    # the clocks / throttle reasons under this kernel's load are on record.
+    sustained = ClockSampler(local, period_ms=50)
+    sustained.start()
+    t_end = time.time() + 0.6
+    while time.time() < t_end:
+        for _ in range(50):
+            step()
+        torch.cuda.synchronize(dev)
+    clk_sustained = sustained.stop()
+    # parity spot-check of the final state on rank 0 (first 2,048 rows vs the oracle)
+    if rank == 0 and not args.no_check:
+        hs = h[:2048].float().cpu().numpy()
+        _, t_ref, m_ref = O.route_logits(hs, orouter)
+        ok = O.decision_band_ok(mask[:2048].cpu().numpy(), t_ref, m_ref, THETA, 2e-2)
+        assert ok.all(), "bench parity spot-check failed"
+        e_ref, _ = O.compact_indices(mask.cpu().numpy())
+        assert np.array_equal(exit_idx[: int(counts[0])].cpu().numpy(), e_ref)
     # per-launch kernel time of the fused kernel alone (events bracket each launch,
     # separate pass so the headline region has no per-step event records)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -368,6 +380,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": N_TOK * 1 + N_TOK * 8 + 16},
             "gpu_launches": gpu_launches,
             "clocks": clk,
+            "clocks_sustained": dict(clk_sustained, window="0.6 s of the same step back to back, "
+                                                          "after the timed region"),
             "extra": {"tensor_cores": bool(lib.tide_route_uses_tensor_cores(N.BF16, D, B)),
                       "tflops_tensor": 2.0 * D * B * N_TOK / (kavg / 1e3) / 1e12,
                       "kernel_ms_min": min(kernel_ms), "kernel_ms_max": max(kernel_ms)},

@@ -231,3 +231,72 @@ def test_split_and_persistent_agree_with_oracle(d, b, n, dtype, monkeypatch):
         np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
         out[mode] = r["logits"].cpu().numpy()
     np.testing.assert_allclose(out["1"], out["0"], rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("n,gathered", [(100_000, False), (160_000, False), (90_000, True)])
+def test_multi_group_persistent_ctas(n, gathered):
+    """More rows than one group per SM (148 x 512): CTAs loop over several
+    groups (accumulator reuse, ring phases carried across groups, epilogue of
+    group g overlapping group g+1's first chunks)."""
+    need_gpu()
+    import torch
+    g = np.random.Generator(np.random.PCG64(4242 + n))
+    d, b = 256, 128
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.05).astype(np.float32)
+    rows = 2 * n if gathered else n
+    h = O.round_to(g.standard_normal((rows, d), dtype=np.float32), "bf16")
+    hd = to_dev(h, "bf16")
+    router = _router(wd, wu)
+    if gathered:
+        idx = np.sort(g.choice(rows, size=n, replace=False)).astype(np.int64)
+        wdd, wud = P.router_ops.device_weights(router, N.BF16, hd.device)
+        it = torch.from_numpy(idx).cuda()
+        r = {k: torch.empty(n, dtype=t, device="cuda") for k, t in
+             (("logits", torch.float32), ("mask", torch.uint8), ("exiting_indices", torch.int64),
+              ("continuing_indices", torch.int64))}
+        counts = torch.empty(2, dtype=torch.int64, device="cuda")
+        N.check(N.load().tide_route(hd.data_ptr(), d, n, None, rows, d, N.BF16, it.data_ptr(),
+                                    wdd.data_ptr(), wud.data_ptr(), b, 1e-6, 0.5, 9, None,
+                                    r["logits"].data_ptr(), r["mask"].data_ptr(),
+                                    r["exiting_indices"].data_ptr(),
+                                    r["continuing_indices"].data_ptr(), 0, None,
+                                    counts.data_ptr(), D.workspace().data_ptr(),
+                                    D.stream_handle()), "tide_route")
+        ne = int(counts[0])
+        r["exiting_indices"] = r["exiting_indices"][:ne]
+        r["continuing_indices"] = r["continuing_indices"][: n - ne]
+        hsel = h[idx]
+    else:
+        r = P.route(hd, router, theta=0.5, want_logits=True, want_indices=True)
+        hsel = h
+    _, t_ref, m_ref = O.route_logits(hsel, O.OracleRouter(3, wd, wu))
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, "bf16", f"n={n}")
+    mask = r["mask"].cpu().numpy()
+    assert O.decision_band_ok(mask, t_ref, m_ref, 0.5, 2e-2).all()
+    e, c = O.compact_indices(mask)
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+def test_headline_shape_full_size():
+    """The bench workload itself: 65,536 x 4096 bf16, one checkpoint.  Logits
+    on a 4,096-row sample; every decision by the band rule; compaction exact."""
+    need_gpu()
+    import torch
+    g = np.random.Generator(np.random.PCG64(202))
+    orouter = O.make_router(4096, 128, 3, g)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1234)
+    hd = torch.randn((65536, 4096), generator=gen, device="cuda").to(torch.bfloat16)
+    r = P.route(hd, P.Router(3, orouter.w_down, orouter.w_up), theta=0.5, want_logits=True,
+                want_indices=True)
+    h = hd.float().cpu().numpy()
+    _, t_ref, m_ref = O.route_logits(h, orouter)
+    logits = r["logits"].cpu().numpy()
+    check_logits(logits[:4096], t_ref[:4096], m_ref[:4096], "bf16", "headline sample")
+    mask = r["mask"].cpu().numpy()
+    assert O.decision_band_ok(mask, t_ref, m_ref, 0.5, 2e-2).all()
+    e, c = O.compact_indices(mask)
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)

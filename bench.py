@@ -237,16 +237,20 @@ def run_ours(args):
     gen.manual_seed(1234 + rank)
     h = torch.randn((N_TOK, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
     wd, wu = P.router_ops.device_weights(router, N.BF16, dev)
+    gathered = S.ExitMapGather(N_TOK, world, dev) if world > 1 else None
     scores = torch.empty(N_TOK, dtype=torch.float32, device=dev)
-    mask = torch.empty(N_TOK, dtype=torch.uint8, device=dev)
-    exit_idx = torch.empty(N_TOK, dtype=torch.int64, device=dev)
     cont_idx = torch.empty(N_TOK, dtype=torch.int64, device=dev)
-    counts = torch.empty(2, dtype=torch.int64, device=dev)
+    if gathered is not None:
+        # the kernel writes straight into the packed all-gather send buffer
+        mask, exit_idx, counts = gathered.exit_map, gathered.exit_idx, gathered.counts
+    else:
+        mask = torch.empty(N_TOK, dtype=torch.uint8, device=dev)
+        exit_idx = torch.empty(N_TOK, dtype=torch.int64, device=dev)
+        counts = torch.empty(2, dtype=torch.int64, device=dev)
     lib = N.load()
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     ws = Dv.workspace(dev).data_ptr()
-    gathered = S.ExitMapGather(N_TOK, world, dev) if world > 1 else None
     launches = {"n": 0}
 
     def step(kernel_events=None):
@@ -262,7 +266,7 @@ def run_ours(args):
         if rc:
             N.check(rc, "tide_route")
         if gathered is not None:
-            gathered.all_gather(mask, exit_idx, counts, rank)
+            gathered.all_gather()  # C1 + C2 in one collective
 
     def barrier():
         if world > 1:

@@ -28,30 +28,46 @@ def shard_range(n: int, rank: int, world: int) -> tuple:
 
 
 class ExitMapGather:
-    """Preallocated C1/C2 all-gathers for equal shards of n_local tokens."""
+    """C1 + C2 as ONE all-gather per step for equal shards of n_local tokens.
 
-    def __init__(self, n_local: int, world: int, device, exit_map_dtype=torch.uint8, group=None):
+    Each rank's send buffer packs [counts int64 x2 | exit indices int64 x
+    n_local | exit map u8 x n_local]; the route kernel writes its outputs
+    straight into those views (`counts`, `exit_idx`, `exit_map`), so the
+    exchange is a single collective with no packing copies."""
+
+    def __init__(self, n_local: int, world: int, device, group=None):
         self.n_local = n_local
         self.world = world
         self.group = group
-        self.exit_map = torch.empty(world * n_local, dtype=exit_map_dtype, device=device)
-        self.counts = torch.empty(world * 2, dtype=torch.int64, device=device)
-        self.indices = torch.empty(world * n_local, dtype=torch.int64, device=device)
+        self.nbytes = 16 + 8 * n_local + ((n_local + 15) // 16) * 16
+        self.send = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+        self.recv = torch.empty(world * self.nbytes, dtype=torch.uint8, device=device)
+        self.counts = self.send[:16].view(torch.int64)
+        self.exit_idx = self.send[16:16 + 8 * n_local].view(torch.int64)
+        self.exit_map = self.send[16 + 8 * n_local:16 + 9 * n_local]
 
-    def all_gather(self, local_exit_map, local_exit_idx, local_counts, rank=None):
-        dist.all_gather_into_tensor(self.exit_map, local_exit_map.contiguous(), group=self.group)
-        dist.all_gather_into_tensor(self.counts, local_counts.contiguous(), group=self.group)
-        dist.all_gather_into_tensor(self.indices, local_exit_idx.contiguous(), group=self.group)
+    def all_gather(self, async_op: bool = False):
+        return dist.all_gather_into_tensor(self.recv, self.send, group=self.group,
+                                           async_op=async_op)
+
+    def _rank_views(self, r):
+        base = r * self.nbytes
+        blk = self.recv[base:base + self.nbytes]
+        return (blk[:16].view(torch.int64), blk[16:16 + 8 * self.n_local].view(torch.int64),
+                blk[16 + 8 * self.n_local:16 + 9 * self.n_local])
+
+    def global_exit_map(self) -> torch.Tensor:
+        """C1: the exit map of all ranks' shards, in token order."""
+        return torch.cat([self._rank_views(r)[2] for r in range(self.world)])
 
     def global_exit_indices(self) -> torch.Tensor:
-        """Concatenate the per-rank stable exit lists with rank offsets (C2)."""
+        """C2: concatenate the per-rank stable exit lists with rank offsets."""
         parts = []
-        counts = self.counts.view(self.world, 2).cpu()
         for r in range(self.world):
-            k = int(counts[r, 0])
-            seg = self.indices[r * self.n_local: r * self.n_local + k]
-            parts.append(seg + r * self.n_local)
-        return torch.cat(parts) if parts else self.indices[:0]
+            cnt, idx, _ = self._rank_views(r)
+            k = int(cnt[0])
+            parts.append(idx[:k] + r * self.n_local)
+        return torch.cat(parts) if parts else self.exit_idx[:0]
 
 
 def assemble_partition(local_lists, local_counts, offsets):

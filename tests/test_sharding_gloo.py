@@ -38,12 +38,13 @@ def _worker(rank, world, port, n, seed, q):
         n_local = s1 - s0
         if n % world == 0:
             gat = S.ExitMapGather(n_local, world, "cpu")
-            ex = torch.zeros(n_local, dtype=torch.int64)
-            ex[: len(e)] = torch.from_numpy(e)
-            gat.all_gather(torch.from_numpy(local_mask.astype(np.uint8)), ex,
-                           torch.tensor([len(e), len(c)], dtype=torch.int64))
+            # what tide_route writes into the packed send buffer's views
+            gat.exit_idx[: len(e)] = torch.from_numpy(e)
+            gat.exit_map.copy_(torch.from_numpy(local_mask.astype(np.uint8)))
+            gat.counts.copy_(torch.tensor([len(e), len(c)], dtype=torch.int64))
+            gat.all_gather()
             glob_exit = gat.global_exit_indices().numpy()
-            glob_map = gat.exit_map.numpy().astype(bool)
+            glob_map = gat.global_exit_map().numpy().astype(bool)
         else:
             glob_exit = None
             glob_map = None

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -56,7 +57,33 @@ __global__ void __launch_bounds__(kLThreads) cos_label_kernel(const __grid_const
         hp[c] = (cb + c < p.C) ? reinterpret_cast<const T*>(p.ck[cb + c]) + i * p.ld : nullptr;
       }
       const bool first = cb == 0;
-      if (vec) {
+      if (vec && sizeof(T) == 2) {
+        // bf16 / f16: mixed-precision FMAs straight on the packed pairs
+        constexpr bool kB = sizeof(T) == 2 && !std::is_same<T, __half>::value;
+        for (int k = lane * V; k < p.d; k += 32 * V) {
+          const uint4 fr = ld_nc_v4(f + k);
+          const uint32_t fw[4] = {fr.x, fr.y, fr.z, fr.w};
+          if (first) {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) dot2_acc<kB>(fw[w], fw[w], ssf);
+          }
+          uint4 raw[kLBatch];
+#pragma unroll
+          for (int c = 0; c < kLBatch; ++c)
+            if (hp[c]) raw[c] = ld_nc_v4(hp[c] + k);
+#pragma unroll
+          for (int c = 0; c < kLBatch; ++c) {
+            if (hp[c]) {
+              const uint32_t hw[4] = {raw[c].x, raw[c].y, raw[c].z, raw[c].w};
+#pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                dot2_acc<kB>(hw[w], fw[w], dot[c]);
+                dot2_acc<kB>(hw[w], hw[w], ssh[c]);
+              }
+            }
+          }
+        }
+      } else if (vec) {
         for (int k = lane * V; k < p.d; k += 32 * V) {
           float fv[V];
           unpack16(ld_nc_v4(f + k), fv, (const T*)nullptr);

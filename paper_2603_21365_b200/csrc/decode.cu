@@ -608,7 +608,10 @@ int launch_cluster(K kernel, const DecParams& p, size_t smem, cudaStream_t s) {
       kmax[i] = smem;
     }
   }
-  if (ok_for < p.C) return 1;  // not co-resident: caller falls back
+  // The resolution is by ticket, so clusters need not all be co-resident, but
+  // a straggler wave costs more than a narrower split (measured: 16-CTA
+  // clusters with 7 of 9 resident 11.0 us vs 8-CTA clusters all resident 10.1)
+  if (ok_for < p.C) return 1;  // caller tries the next split / falls back
   cudaLaunchKernelEx(&cfg, kernel, p);
   return check_launch("decode_tc_kernel (cluster)") == TIDE_OK ? 0 : -1;
 }

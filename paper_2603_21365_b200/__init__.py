@@ -15,8 +15,8 @@ from .calibration import (CalibrationConfig, CalibrationDataset, CollectedStates
 from .router_ops import (SMALL_BATCH_CUTOVER, CompactionResult, Router, batch_compact,
                          exit_projection, exit_scatter, fused_layernorm_route, route,
                          route_logits, route_scores)
-from .runtime import (BATCH_UNANIMOUS, FINAL_KEY, MODES, NO_EXIT, PER_TOKEN, OutputHead,
-                      PhaseStats, RuntimeConfig, posthoc_select, select_exits)
+from .runtime import (BATCH_UNANIMOUS, FINAL_KEY, MODES, NO_EXIT, PER_TOKEN, DecodeStep,
+                      OutputHead, PhaseStats, RuntimeConfig, posthoc_select, select_exits)
 from .tensor_math import DEFAULT_EPS, batched_cosine_similarity
 
 __version__ = "0.1.0"
@@ -26,7 +26,8 @@ __all__ = [
     "checkpoint_layers", "compute_labels", "label_tensors", "make_bank",
     "SMALL_BATCH_CUTOVER", "CompactionResult", "Router", "batch_compact", "exit_projection",
     "exit_scatter", "fused_layernorm_route", "route", "route_logits", "route_scores",
-    "BATCH_UNANIMOUS", "FINAL_KEY", "MODES", "NO_EXIT", "PER_TOKEN", "OutputHead", "PhaseStats",
+    "BATCH_UNANIMOUS", "FINAL_KEY", "MODES", "NO_EXIT", "PER_TOKEN", "DecodeStep", "OutputHead",
+    "PhaseStats",
     "RuntimeConfig", "posthoc_select", "select_exits",
     "DEFAULT_EPS", "batched_cosine_similarity", "__version__",
     "load_bank", "save_bank", "bank_file_size", "install_device_weights", "BinaryFormatError",

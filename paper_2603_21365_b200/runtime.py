@@ -257,6 +257,58 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
     return exit_layers
 
 
+class DecodeStep:
+    """The decode-step exit decision with everything bound once.
+
+    For serving loops whose checkpoint captures live in static buffers (a
+    CUDA-graph-captured decode step, or `CheckpointCapture` output reused per
+    step): validation, the decode plan, the ctypes argument block and the
+    output buffer are built here, so each call is one `tide_route_decode`
+    launch (~10x less host time than `select_exits`' checks, see
+    tools/host_overhead.py).  Same result as `select_exits(hidden_states, bank,
+    config)` for those buffers' current contents.
+
+        step = DecodeStep(hidden_states, bank, cfg)   # n <= 16 rows
+        exits = step()       # int64 [n] CUDA tensor, rewritten by every call
+
+    The launch goes to the CUDA stream current at construction.  Re-create
+    the object if a router of the bank is replaced."""
+
+    def __init__(self, hidden_states, bank, config: RuntimeConfig, *, out=None):
+        L = bank.num_layers
+        ckpts = [k for k in bank.checkpoints if k >= config.k_min]
+        if not ckpts:
+            raise ValueError("DecodeStep needs at least one checkpoint >= k_min")
+        staged, dev = _stage_layers(hidden_states, [k + 1 for k in ckpts] + [L])
+        n, d = staged[L].shape
+        code = D.dtype_code(staged[L])
+        vec = 4 if code == N.F32 else 8
+        if not (1 <= n <= N.MAX_DECODE_ROWS) or d % vec or any(
+                staged[k + 1].data_ptr() % 16 for k in ckpts):
+            raise ValueError(f"DecodeStep needs 1..{N.MAX_DECODE_ROWS} rows, d % {vec} == 0 "
+                             "and 16-byte aligned captures")
+        if any(staged[k + 1] is not hidden_states[k + 1] for k in ckpts):
+            raise ValueError("DecodeStep needs the captures as contiguous CUDA tensors of one "
+                             "dtype (a converted copy would not see later writes)")
+        self.out = out if out is not None else torch.empty((n,), dtype=torch.int64, device=dev)
+        w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)
+        b = bank.bottleneck if hasattr(bank, "bottleneck") else bank.routers[ckpts[0]].bottleneck
+        s = D.stream_handle(dev)
+        mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
+        self._keep = (staged, w_arr, u_arr, l_arr, bank)
+        self._fn = N.load().tide_route_decode
+        self._args = (N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n,
+                      d, code, w_arr, u_arr, b, l_arr, float(np.float32(bank.eps)),
+                      float(np.float32(config.exit_threshold)), int(config.k_min), mode, None,
+                      None, self.out.data_ptr(), None, D.workspace(dev, s).data_ptr(), s)
+
+    def __call__(self) -> torch.Tensor:
+        rc = self._fn(*self._args)
+        if rc:
+            N.check(rc, "tide_route_decode")
+        return self.out
+
+
 def posthoc_select(model, hidden_states, bank, config: RuntimeConfig, *,
                    return_logits: bool = True):
     """Select output logits per the post-hoc exit rule (ee/runtime.py:134-181).

@@ -213,3 +213,23 @@ def test_rigged_hot_bf16_device_exact():
     assert e[17] == P.NO_EXIT and np.all(np.delete(e, 17) == 7)
     _, exits = P.posthoc_select(head, states, bank, P.RuntimeConfig(exit_threshold=1.0))
     assert np.all(exits.cpu().numpy() == P.NO_EXIT)
+
+
+@pytest.mark.parametrize("mode", [P.PER_TOKEN, P.BATCH_UNANIMOUS])
+def test_decode_step_object_matches_select_exits(mode):
+    """DecodeStep (bound once, static buffers) == select_exits on the same
+    buffers, including after the buffers are rewritten in place."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(36, 4096, 8, "bf16", 31, scale=0.3)
+    cfg = P.RuntimeConfig(exit_threshold=0.55, mode=mode)
+    step = P.DecodeStep(states, bank, cfg)
+    for it in range(3):
+        if it:
+            g = torch.Generator(device="cuda")
+            g.manual_seed(100 + it)
+            for k in ckpts:
+                states[k + 1].copy_(torch.randn(states[k + 1].shape, generator=g,
+                                                device="cuda").to(states[k + 1].dtype))
+        got = step().clone()
+        want = P.select_exits(states, bank, cfg)
+        assert torch.equal(got, want)

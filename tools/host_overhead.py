@@ -29,3 +29,14 @@ for _ in range(2000):
 pr.disable()
 torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+step = P.DecodeStep(states, bank, cfg)
+for _ in range(50):
+    step()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(2000):
+    step()
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"DecodeStep host time per call: {(t1 - t0) / 2000 * 1e6:.1f} us")

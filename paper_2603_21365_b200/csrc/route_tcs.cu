@@ -534,6 +534,9 @@ void tcs_set_attrs(int dev) {
   if (!attr_set[dev & 63]) {
     cudaFuncSetAttribute(route_tcs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(route_tcs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // clusters of 16 (the chain's links with a handful of live rows)
+    cudaFuncSetAttribute(route_tcs_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(route_tcs_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set[dev & 63] = true;
   }
 }
@@ -541,8 +544,8 @@ void tcs_set_attrs(int dev) {
 // Co-resident clusters of size c (a cluster lives in one GPC, so this is less
 // than SMs / c: e.g. clusters of 8 leave several SMs of every GPC idle).
 int tcs_max_clusters(int dev, int c, uint32_t smem) {
-  static int cache[64][4][2];  // [dev][c = 2, 4, 8][smem class]
-  const int ci = c == 2 ? 0 : c == 4 ? 1 : 2;
+  static int cache[64][4][2];  // [dev][c = 2, 4, 8, 16][smem class]
+  const int ci = c == 2 ? 0 : c == 4 ? 1 : c == 8 ? 2 : 3;
   const int si = smem > 200 * 1024 ? 1 : 0;
   int& mc = cache[dev & 63][ci][si];
   if (!mc) {
@@ -579,19 +582,20 @@ int tcs_max_clusters(int dev, int c, uint32_t smem) {
 // whose co-resident CTAs cover every tile of the capacity at split 1 — the
 // kernel picks the split from the live count (a link that still holds most
 // rows runs at split 1-2 on fewer SMs; the links after a large exit wave run
-// at split 8).  C in {2, 4, 8}: bp / C a multiple of 16 and
-// at least one 64-column k-chunk per rank.
+// at split 8-16).  C in {2, 4, 8} (16 for chain links: a non-portable
+// cluster size, so links with a handful of live rows stream 1/16 of W per
+// CTA): bp / C a multiple of 8 and at least one 64-column k-chunk per rank.
 int route_tcs_plan(const RouteArgs& a, int dev, int* grid) {
   // TIDE_SPLIT: "0" forces the persistent K1, 2/4/8 caps the split (tests, sweeps)
   const char* env = getenv("TIDE_SPLIT");
-  const int cap = env ? atoi(env) : 8;
+  const int cap = env ? atoi(env) : 16;
   TcsLayout L;
   if (cap <= 1 || a.n < 1 || !tcs_layout(a.b, L)) return 0;
   const int64_t tiles = (a.n + 127) / 128;
   const int nk = (a.d + 63) / 64;
   const bool live = a.n_dev != nullptr;
-  for (int c = 8; c >= 2; c >>= 1) {
-    if (c > cap || c > nk || L.bp % (16 * c) != 0) continue;
+  for (int c = 16; c >= 2; c >>= 1) {
+    if (c > cap || c > nk || L.bp % (8 * c) != 0 || (c == 16 && !live)) continue;
     const int64_t mc = tcs_max_clusters(dev, c, L.smem_bytes);
     if (!live && tiles <= mc) {
       *grid = (int)(tiles * c);

@@ -211,7 +211,13 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   const int k0 = (int)((int64_t)p.nk * rank / ks), k1 = (int)((int64_t)p.nk * (rank + 1) / ks);
   const bool gathered = p.row_idx != nullptr;
 
-  if (warp == 0 && lane == 0) {
+  // Rank j owns rows [j R, (j+1) R) of the tile in the reduction; ranks whose
+  // rows are all past the tile's live rows exchange and finish nothing (a chain
+  // link with a handful of rows: one live rank instead of 16).
+  const int Rr = 128 / ks;
+  const int live_rows = (int)(r1 - r0);
+  const bool live_rank = (int)rank * Rr < live_rows;
+  if (warp == 0 && lane == 0 && live_rank) {
     // ks - 1 bulk copies of [bp + 1][128 / ks] floats land here (complete_tx may
     // precede this expect_tx: the phase needs the arrive as well)
     mbar_arrive_expect_tx(recv_full, (uint32_t)(ks - 1) * (uint32_t)(p.bp + 1) * (512u / ks));
@@ -221,6 +227,20 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TL(1);
+  // Row ids needed on the tail (exit-layer scatter by the finishing threads,
+  // index writes by warp 2) are loaded now, while the stream runs: no
+  // dependent global loads after the reduction.
+  const int64_t pr0e = r0 + (int64_t)rank * Rr;
+  const int64_t pr1e = (pr0e + Rr < r1) ? pr0e + Rr : (pr0e < r1 ? r1 : pr0e);
+  const int tf = threadIdx.x - 64;
+  const int64_t fin_id =
+      (gathered && tf >= 0 && tf < Rr && pr0e + tf < pr1e) ? p.row_idx[pr0e + tf] : pr0e + tf;
+  int64_t wr_id[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int64_t r = pr0e + 32 * w + lane;
+    wr_id[w] = (warp == 2 && gathered && p.ids_from_rows && 32 * w < Rr && r < pr1e) ? p.row_idx[r] : r;
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------- producer
@@ -342,12 +362,15 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     const int jo = row / R, rr = row - jo * R;
     float* so = stage_out + (size_t)jo * p.bp * R + rr;
     const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16);
-    for (int c0 = 0; c0 < p.bp; c0 += 32) {
+    const bool warp_live = (32 * q) / R * R < live_rows;  // some destination of this warp's rows is live
+    for (int c0 = 0; warp_live && c0 < p.bp; c0 += 32) {
       uint32_t v[32];
       tmem_ld32(taddr + (uint32_t)c0, v);
       tmem_ld_wait();
+      if (jo * R < live_rows) {
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) so[(size_t)(c0 + jj) * R] = __uint_as_float(v[jj]);
+        for (int jj = 0; jj < 32; ++jj) so[(size_t)(c0 + jj) * R] = __uint_as_float(v[jj]);
+      }
     }
     float* stage_ss = stage_out + (size_t)p.bp * 128;
     stage_ss[row] = ssp;
@@ -359,6 +382,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       const uint32_t blk = (uint32_t)p.bp * (uint32_t)R * 4u;
       for (uint32_t j = 0; j < (uint32_t)ks; ++j) {
         if (j == rank) continue;  // own rows are read from stage_out in place
+        if ((int)j * R >= live_rows) break;  // dead ranks (and all after them) get nothing
         const uint32_t bar = dsmem_addr(smem_u32(recv_full), gbase + j);
         bulk_s2dsmem(dsmem_addr(smem_u32(recv) + rank * blk, gbase + j), smem_u32(stage_out) + j * blk,
                      blk, bar);
@@ -375,7 +399,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   }
 
   if (warp >= 2) {
-    mbar_wait(recv_full, 0);
+    if (live_rank) mbar_wait(recv_full, 0);
     // every copy INTO this CTA has landed; once all CTAs arrive, every copy
     // FROM this CTA's smem has been read, so it may exit
     cluster_arrive_relaxed();
@@ -398,7 +422,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     // (one warp per SMSP here, so ILP is what hides the latency)
     f32x2 acc2 = 0ull, acc2b = 0ull;
     const int cbase = sl * cw;
-    for (int cl0 = 0; cl0 < cw; cl0 += 8) {
+    for (int cl0 = 0; live_rank && cl0 < cw; cl0 += 8) {
       if (cbase + cl0 >= p.b) break;
       float sum[8];
 #pragma unroll
@@ -440,7 +464,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         if (p.scores) p.scores[r] = score;
         if (p.logits) p.logits[r] = logit;
         if (p.mask) p.mask[r] = ex ? 1 : 0;
-        if (ex && p.exit_layers) p.exit_layers[gathered ? p.row_idx[r] : r] = p.layer;
+        if (ex && p.exit_layers) p.exit_layers[fin_id] = p.layer;
       }
     }
     const uint32_t bal = __ballot_sync(0xffffffffu, ex);
@@ -463,13 +487,15 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       if (lane == 0) TL(8);
       if (p.exit_idx || p.cont_idx) {
         const uint32_t lt = (1u << lane) - 1u;
-        for (int w = 0; w < nw; ++w) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          if (w >= nw) break;
           const uint32_t wd = __shfl_sync(0xffffffffu, word, w);
           const uint32_t pre = __shfl_sync(0xffffffffu, excl_w, w);
           const int64_t r = pr0 + 32 * w + lane;
           if (r < pr1) {
             const int64_t rank_e = (int64_t)E + pre + __popc(wd & lt);
-            const int64_t id = (p.ids_from_rows && gathered) ? p.row_idx[r] : r;
+            const int64_t id = wr_id[w];
             if ((wd >> lane) & 1u) {
               if (p.exit_idx) p.exit_idx[rank_e] = id;
             } else if (p.cont_idx) {

@@ -13,6 +13,9 @@ P.label_tensors(cks, fin, 0.98, labels_dtype="u8")
 # decode step (config 3)
 ckpts, states, bank = BE._case(36, 4096, 8, torch.bfloat16, 3, 0.3)
 P.select_exits(states, bank, P.RuntimeConfig(exit_threshold=0.5))
+# peeling chain at the config 2 shape (split-K cluster kernel, 8 links)
+ckpts, states, bank = BE._case(32, 4096, 4096, torch.bfloat16, 2, 0.1)
+P.select_exits(states, bank, P.RuntimeConfig(exit_threshold=0.5))
 # posthoc output staging + compaction + CUDA-core route (config 1, f32)
 g = np.random.Generator(np.random.PCG64(42))
 routers = {k: O.make_router(768, 128, k, g) for k in (3, 7, 11)}

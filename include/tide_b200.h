@@ -154,6 +154,27 @@ int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_
                       int32_t mode, float* scores, float* logits, int64_t* exit_layers,
                       int64_t* exit_count, void* workspace, void* stream);
 
+/*
+ * Tail of a per-token peeling chain (ee/runtime.py:166-178) in ONE routing
+ * launch: after some links of the chain, the rows still live (row_idx[0 .. *n_dev),
+ * device memory, as written by tide_route's cont_idx / counts[1]) are scored
+ * against the C remaining checkpoints at once (checkpoint c: captures
+ * h_ptrs[c], router w_ptrs[c] / wup_ptrs[c], layer layers[c]; HOST pointer
+ * arrays, ascending layers) and each row gets the first checkpoint whose
+ * score > theta in exit_layers[row id].  Only when *n_dev <= n_limit; else
+ * nothing is routed.  *tail_count receives the live count the following
+ * links must read (0 when the tail handled the rows, else *n_dev), so links
+ * launched after it with n_dev = tail_count become no-ops.  scores: device
+ * scratch of C * cap f32 (cap = the chain's row capacity).  bf16 / f16.
+ * (No reference counterpart: an execution strategy of posthoc_select.)
+ */
+int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t rows_total,
+                    int32_t d, int32_t dtype, const int64_t* row_idx, const int64_t* n_dev,
+                    int64_t cap, int64_t n_limit, const void* const* w_ptrs,
+                    const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
+                    float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
+                    void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

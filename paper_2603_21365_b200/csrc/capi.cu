@@ -125,6 +125,46 @@ int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int
   return route_simt_launch(a, s);
 }
 
+int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t rows_total,
+                    int32_t d, int32_t dtype, const int64_t* row_idx, const int64_t* n_dev,
+                    int64_t cap, int64_t n_limit, const void* const* w_ptrs,
+                    const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
+                    float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
+                    void* workspace, void* stream) {
+  if (C < 1 || !h_ptrs || !w_ptrs || !wup_ptrs || !layers)
+    return set_error(TIDE_ERR_ARG, "tide_route_tail: bad checkpoint arrays");
+  if (d < 1 || b < 1 || cap < 1 || ld_h < d || rows_total < 1 || n_limit < 0)
+    return set_error(TIDE_ERR_ARG, "tide_route_tail: bad shape");
+  if (!row_idx || !n_dev || !scores || !exit_layers || !tail_count || !workspace)
+    return set_error(TIDE_ERR_ARG, "tide_route_tail: null device buffer");
+  if (dtype != TIDE_F16 && dtype != TIDE_BF16)
+    return set_error(TIDE_ERR_UNSUPPORTED, "tide_route_tail: bf16 / f16 captures only");
+  if (!route_tc_supported(dtype, d, b)) return set_error(TIDE_ERR_UNSUPPORTED, "tide_route_tail: shape");
+  for (int c = 0; c < C; ++c)
+    if (((reinterpret_cast<uintptr_t>(h_ptrs[c]) | reinterpret_cast<uintptr_t>(w_ptrs[c])) & 15) ||
+        (c && layers[c] <= layers[c - 1]))
+      return set_error(TIDE_ERR_ARG, "tide_route_tail: unaligned pointer or unordered layers");
+  RouteArgs a{};
+  a.h = h_ptrs[0];
+  a.ld_h = ld_h;
+  a.n = cap;
+  a.n_dev = n_dev;
+  a.rows_total = rows_total;
+  a.d = d;
+  a.dtype = dtype;
+  a.row_idx = row_idx;
+  a.w_down = w_ptrs[0];
+  a.w_up = wup_ptrs[0];
+  a.b = b;
+  a.eps = eps;
+  a.theta = theta;
+  a.scores = scores;
+  a.exit_layers = exit_layers;
+  a.workspace = workspace;
+  return route_tcs_tail_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, layers, n_limit, tail_count,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
 int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
                  int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
                  int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,

@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -39,7 +40,23 @@ constexpr int kThreadsS = 192;  // producer, MMA issuer, 4 RMS / epilogue warps
 constexpr int kMaxStages = 8;
 constexpr int kASlot = 128 * 128;  // 128 rows x 64 cols x 2 B
 
+constexpr int kMaxTailC = 32;  // checkpoints of one chain-tail launch (grid.y)
+struct TailLayers {
+  int64_t l[kMaxTailC];
+};
+
+template <int NC>
+struct WMaps {  // W_down tensor map per checkpoint (NC = 1: the plain route)
+  CUtensorMap m[NC];
+};
+
 struct SplitParams {
+  // chain tail (NC > 1): checkpoint c = blockIdx.y reads its rows from
+  // h_bases[c] and w_ups[c] and writes scores[c * cap + position]; the launch
+  // does nothing when the live count exceeds n_limit
+  const uint8_t* h_bases[kMaxTailC];
+  const float* w_ups[kMaxTailC];
+  int64_t cap, n_limit;
   int64_t n_host;
   const int64_t* n_dev;
   int64_t rows_total;
@@ -129,10 +146,15 @@ __device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
-template <bool kBF16>
+template <bool kBF16, int NC>
 __global__ void __launch_bounds__(kThreadsS, 1)
-    route_tcs_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_w,
+    route_tcs_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ WMaps<NC> wm,
                      const __grid_constant__ SplitParams p) {
+  const int ck = NC > 1 ? (int)blockIdx.y : 0;
+  const CUtensorMap& tm_w = wm.m[ck];
+  const uint8_t* const h_base = NC > 1 ? p.h_bases[ck] : p.h_base;
+  const float* const w_up_c = NC > 1 ? p.w_ups[ck] : p.w_up;
+  float* const scores_c = (NC > 1 && p.scores) ? p.scores + (size_t)ck * p.cap : p.scores;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // partials of this CTA's rows from the ks ranks: [src][bp][R], then ss [src][R]
@@ -180,7 +202,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   griddep_wait();
   const uint32_t crank = cluster_rank();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
-  const int64_t ntiles = (n + 127) / 128;
+  const int64_t ntiles = (NC > 1 && n > p.n_limit) ? 0 : (n + 127) / 128;  // tail: over the limit -> idle
   int ks = p.ks;
   while (ks > 1 && ntiles * ks > (int64_t)gridDim.x) ks >>= 1;
   const uint32_t rank = crank % (uint32_t)ks, gbase = crank - rank;
@@ -317,7 +339,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
           const int rw = 32 * q + 4 * it + rg;
           if (src_off[it] >= 0)
             cp_async16(dst + rw * 128 + ((sub ^ (rw & 7)) << 4),
-                       p.h_base + src_off[it] + (in ? c * 2 : 0), in ? 16u : 0u);
+                       h_base + src_off[it] + (in ? c * 2 : 0), in ? 16u : 0u);
         }
       }
       cp_async_arrive_noinc(&full[si]);
@@ -347,7 +369,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       if (++s == p.stages) { s = 0; ph ^= 1u; }
     }
     const float ssp = (sq[0] + sq[1]) + (sq[2] + sq[3]);
-    for (int i = threadIdx.x - 64; i < p.b; i += 128) sWup[i] = p.w_up[i];  // used after recv_full
+    for (int i = threadIdx.x - 64; i < p.b; i += 128) sWup[i] = w_up_c[i];  // used after recv_full
     if (warp == 2 && lane == 0) TL(3);
     mbar_wait(acc_full, 0);  // every MMA retired: the stage ring is no longer read by the MMAs
     tc_fence_after();
@@ -461,7 +483,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       if (r < pr1) {
         const float score = score_from_logit(logit);
         ex = score > p.theta;
-        if (p.scores) p.scores[r] = score;
+        if (scores_c) scores_c[r] = score;
         if (p.logits) p.logits[r] = logit;
         if (p.mask) p.mask[r] = ex ? 1 : 0;
         if (ex && p.exit_layers) p.exit_layers[fin_id] = p.layer;
@@ -558,11 +580,15 @@ bool tcs_layout(int b, TcsLayout& L) {
 void tcs_set_attrs(int dev) {
   static bool attr_set[64] = {false};
   if (!attr_set[dev & 63]) {
-    cudaFuncSetAttribute(route_tcs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(route_tcs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    // clusters of 16 (the chain's links with a handful of live rows)
-    cudaFuncSetAttribute(route_tcs_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(route_tcs_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    // clusters of 16 (the chain's links with a handful of live rows) are non-portable
+    auto set = [](auto k) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    };
+    set(route_tcs_kernel<true, 1>);
+    set(route_tcs_kernel<false, 1>);
+    set(route_tcs_kernel<true, kMaxTailC>);
+    set(route_tcs_kernel<false, kMaxTailC>);
     attr_set[dev & 63] = true;
   }
 }
@@ -588,7 +614,7 @@ int tcs_max_clusters(int dev, int c, uint32_t smem) {
     q.attrs = qa;
     q.numAttrs = 1;
     int v = 0;
-    if (cudaOccupancyMaxActiveClusters(&v, route_tcs_kernel<true>, &q) != cudaSuccess || v <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&v, route_tcs_kernel<true, 1>, &q) != cudaSuccess || v <= 0) {
       cudaGetLastError();
       v = sm_count(dev) / (2 * c);
     }
@@ -635,9 +661,10 @@ int route_tcs_plan(const RouteArgs& a, int dev, int* grid) {
   return 0;
 }
 
-int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) {
-  SplitParams p{};
-  TcsLayout L;
+namespace {
+
+// Common parameter block of a split-K launch (layout, numerics, outputs).
+int tcs_params(const RouteArgs& a, int ks, SplitParams& p, TcsLayout& L) {
   if (!tcs_layout(a.b, L)) return set_error(TIDE_ERR_UNSUPPORTED, "split route: smem too small");
   const int npad = L.npad, bp = L.bp;
   p.n_host = a.n;
@@ -660,7 +687,6 @@ int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) 
   p.off_bar = L.off_bar;
   p.off_words = L.off_words;
   p.off_tmem = L.off_tmem;
-  const uint32_t smem_bytes = L.smem_bytes;
   p.row_idx = a.row_idx;
   p.ids_from_rows = a.ids_from_rows;
   p.h_base = reinterpret_cast<const uint8_t*>(a.h);
@@ -679,20 +705,23 @@ int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) 
   p.counts = a.counts;
   p.ws = reinterpret_cast<Workspace*>(a.workspace);
   p.dbg = g_dbg;
-
   const int64_t tiles = (a.n + 127) / 128;
   if (tiles * ks > kMaxParts / 2) return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
-  CUtensorMap tm_h, tm_w;
+  return TIDE_OK;
+}
+
+template <int NC>
+int tcs_launch(const RouteArgs& a, const SplitParams& p, const WMaps<NC>& wm, uint32_t smem_bytes,
+               int ks, int grid, int ny, cudaStream_t stream, const char* what) {
+  CUtensorMap tm_h;
   const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
   int rc;
   if ((rc = make_map(&tm_h, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
-  if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
-
   int dev = 0;
   cudaGetDevice(&dev);
   tcs_set_attrs(dev);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.gridDim = dim3((unsigned)grid, (unsigned)ny, 1);
   cfg.blockDim = dim3(kThreadsS, 1, 1);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
@@ -710,11 +739,117 @@ int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) 
   }
   cudaError_t e;
   if (a.dtype == TIDE_BF16)
-    e = cudaLaunchKernelEx(&cfg, route_tcs_kernel<true>, tm_h, tm_w, p);
+    e = cudaLaunchKernelEx(&cfg, route_tcs_kernel<true, NC>, tm_h, wm, p);
   else
-    e = cudaLaunchKernelEx(&cfg, route_tcs_kernel<false>, tm_h, tm_w, p);
-  if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "route_tcs_kernel: %s", cudaGetErrorString(e));
-  return check_launch("route_tcs_kernel");
+    e = cudaLaunchKernelEx(&cfg, route_tcs_kernel<false, NC>, tm_h, wm, p);
+  if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return check_launch(what);
+}
+
+// Chain tail, step 2: first firing checkpoint of every live row (per-token
+// rule of ee/runtime.py:166-178 over the tail's checkpoints, in order) and the
+// live count the following links read (0 when the tail handled the rows).
+__global__ void chain_resolve_kernel(const float* scores, int64_t cap, int nc, TailLayers layers,
+                                     float theta, const int64_t* n_dev, int64_t n_limit,
+                                     const int64_t* row_idx, int64_t* exit_layers,
+                                     int64_t* tail_count) {
+  griddep_wait();
+  const int64_t n = *n_dev;
+  const bool handled = n <= n_limit;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *tail_count = handled ? 0 : n;
+  if (!handled) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rid = row_idx[i];
+    // 8 checkpoints' scores in flight per step (the loads are independent)
+    for (int c0 = 0; c0 < nc; c0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = c0 + u < nc ? __ldcg(scores + (size_t)(c0 + u) * cap + i) : 0.f;
+      int hit = -1;
+#pragma unroll
+      for (int u = 7; u >= 0; --u)
+        if (c0 + u < nc && v[u] > theta) hit = c0 + u;
+      if (hit >= 0) {
+        exit_layers[rid] = layers.l[hit];
+        break;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) {
+  SplitParams p{};
+  TcsLayout L;
+  int rc;
+  if ((rc = tcs_params(a, ks, p, L))) return rc;
+  WMaps<1> wm;
+  if ((rc = make_map(&wm.m[0], a.w_down, a.dtype, a.d, a.b, a.d, 64, L.npad))) return rc;
+  return tcs_launch<1>(a, p, wm, L.smem_bytes, ks, grid, 1, stream, "route_tcs_kernel");
+}
+
+int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
+                          const void* const* w_ptrs, const float* const* wup_ptrs,
+                          const int64_t* layers, int64_t n_limit, int64_t* tail_count,
+                          cudaStream_t stream) {
+  if (C < 1 || C > kMaxTailC) return set_error(TIDE_ERR_ARG, "tail: C must be in [1, %d]", kMaxTailC);
+  if (!a.row_idx || !a.n_dev || !a.scores || !a.exit_layers || !tail_count)
+    return set_error(TIDE_ERR_ARG, "tail: row_idx, n_dev, scores, exit_layers, tail_count required");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // One wave for every checkpoint at once: X CTAs per checkpoint (a multiple
+  // of the cluster size), and at most X tiles of live rows (n_limit clamp).
+  TcsLayout L0;
+  if (!tcs_layout(a.b, L0)) return set_error(TIDE_ERR_UNSUPPORTED, "tail: smem too small");
+  const int nk = (a.d + 63) / 64;
+  const int per = std::max(1, sm_count(dev) / C);
+  int ks = 1;
+  for (int c = 16; c >= 2; c >>= 1)
+    if (c <= per && c <= nk && L0.bp % (8 * c) == 0 &&
+        tcs_max_clusters(dev, c, L0.smem_bytes) * c >= (per / c) * c * 1) {
+      ks = c;
+      break;
+    }
+  const int grid = std::max(ks, per / ks * ks);
+  n_limit = std::min<int64_t>(n_limit, (int64_t)grid * 128);
+  SplitParams p{};
+  TcsLayout L;
+  int rc;
+  if ((rc = tcs_params(a, ks, p, L))) return rc;
+  p.cap = a.n;
+  p.n_limit = n_limit;
+  p.logits = nullptr;  // scores only; no mask / compaction / exit layers in the routing step
+  p.mask = nullptr;
+  p.exit_idx = nullptr;
+  p.cont_idx = nullptr;
+  p.exit_layers = nullptr;
+  p.counts = nullptr;
+  static WMaps<kMaxTailC> wm;  // host staging (copied into the launch parameters)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int c = 0; c < C; ++c) {
+    p.h_bases[c] = reinterpret_cast<const uint8_t*>(h_ptrs[c]);
+    p.w_ups[c] = wup_ptrs[c];
+    if ((rc = make_map(&wm.m[c], w_ptrs[c], a.dtype, a.d, a.b, a.d, 64, L.npad))) return rc;
+  }
+  if ((rc = tcs_launch<kMaxTailC>(a, p, wm, L.smem_bytes, ks, grid, C, stream, "route_tcs_kernel (tail)")))
+    return rc;
+  TailLayers tl{};
+  for (int c = 0; c < C; ++c) tl.l[c] = layers[c];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((n_limit + 255) / 256, 148)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, chain_resolve_kernel, (const float*)a.scores, (int64_t)a.n, C, tl, a.theta,
+                     a.n_dev, n_limit, a.row_idx, a.exit_layers, tail_count);
+  return check_launch("chain_resolve_kernel");
 }
 
 }  // namespace tide

@@ -245,6 +245,12 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
     rem = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
     cnt = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(2)]
     row_idx, n_dev = 0, 0
+    # Chain tail: after TAIL_AFTER links, the rows still live are scored against
+    # every remaining checkpoint in ONE launch (when few enough: n_limit) and
+    # the remaining links become no-ops — the later links of a peeling chain
+    # hold a handful of rows each, so per-link latency, not bytes, is their cost.
+    tail_at = TAIL_AFTER - 1 if (code != N.F32 and len(ckpts) - TAIL_AFTER >= 2
+                                 and _tail_enabled()) else -1
     for i, k in enumerate(ckpts):
         wd, wu = device_weights(bank.routers[k], code, dev)
         h = staged[k + 1]
@@ -254,7 +260,37 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
                                cnt[i & 1].data_ptr(), ws, s), "tide_route")
         row_idx = rem[i & 1].data_ptr()
         n_dev = cnt[i & 1].data_ptr() + 8
+        if i == tail_at:
+            n_dev = _chain_tail(lib, staged, bank, ckpts[i + 1:], code, dev, n, d, b, eps, theta,
+                                row_idx, n_dev, exit_layers, ws, s)
     return exit_layers
+
+
+TAIL_AFTER = 3  # links of the peeling chain before the tail attempt
+
+
+def _tail_enabled() -> bool:
+    import os
+    return os.environ.get("TIDE_CHAIN_TAIL", "1") != "0"
+
+
+def _chain_tail(lib, staged, bank, rest, code, dev, n, d, b, eps, theta, row_idx, n_dev,
+                exit_layers, ws, s):
+    """tide_route_tail over the remaining checkpoints; returns the live-count
+    pointer the following links read (0 rows when the tail handled them)."""
+    n_limit = int(min(n, max(128, (2048 * 4096) // d)))
+    wts = [device_weights(bank.routers[k], code, dev) for k in rest]
+    scratch = torch.empty(len(rest) * n, dtype=torch.float32, device=dev)
+    tail_count = torch.empty(1, dtype=torch.int64, device=dev)
+    rc = lib.tide_route_tail(
+        N.ptr_array([staged[k + 1].data_ptr() for k in rest]), len(rest), d, n, d, code, row_idx,
+        n_dev, n, n_limit, N.ptr_array([w.data_ptr() for w, _ in wts]),
+        N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(rest), eps, theta,
+        scratch.data_ptr(), exit_layers.data_ptr(), tail_count.data_ptr(), ws, s)
+    if rc:
+        return n_dev  # shape without a split-K plan: the links do the work
+    _chain_tail.keep = (scratch, tail_count)  # alive until the stream reaches them
+    return tail_count.data_ptr()
 
 
 class DecodeStep:

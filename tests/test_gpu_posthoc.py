@@ -233,3 +233,26 @@ def test_decode_step_object_matches_select_exits(mode):
         got = step().clone()
         want = P.select_exits(states, bank, cfg)
         assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("d,n,L,scale,theta", [(4096, 4096, 32, 0.1, 0.5), (8192, 2048, 40, 0.06, 0.7),
+                                               (4096, 1000, 24, 0.2, 0.55)])
+def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch):
+    """The chain tail (one launch for the remaining checkpoints once few rows
+    are live) gives the oracle's first-exit map (band rule), as the plain links do."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(L, d, n, "bf16", 7 + d + n, scale=scale)
+    cfg = P.RuntimeConfig(exit_threshold=theta)
+    scores, exc = {}, np.zeros(n, bool)
+    for k in ckpts:
+        s, t, m = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
+        scores[k] = s
+        exc |= np.abs(t - O.logit_of(theta)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
+    want = O.first_exit_from_scores(scores, theta)
+    out = {}
+    for tail in ("1", "0"):
+        monkeypatch.setenv("TIDE_CHAIN_TAIL", tail)
+        got = P.select_exits(states, bank, cfg).cpu().numpy()
+        assert np.all((got == want) | exc), tail
+        out[tail] = got
+    assert np.all((out["1"] == out["0"]) | exc)

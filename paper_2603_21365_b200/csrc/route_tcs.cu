@@ -215,10 +215,12 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       p.counts[0] = 0;
       p.counts[1] = 0;
     }
-    cluster_arrive_relaxed();
-    cluster_wait();
-    cluster_arrive_relaxed();
-    cluster_wait();
+    if (ntiles > 0) {  // some group of the cluster may be live: keep its barrier count
+      cluster_arrive_relaxed();
+      cluster_wait();
+      cluster_arrive_relaxed();
+      cluster_wait();
+    }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {

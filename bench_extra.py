@@ -147,8 +147,10 @@ def config1():
     bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=12)
     cfg = P.RuntimeConfig(exit_threshold=0.5)
     ms = _time(lambda: P.select_exits(states, bank, cfg))
+    gms = _graph_time(lambda: P.select_exits(states, bank, cfg))
     return {"config": "1: GPT-2-small shape, L=12 (3 ckpts), d=768, 2,048 tok, fp32 (CUDA-core "
-                      "path, f32 products)", "ms": ms, "tokens_per_s": 2048 / (ms / 1e3)}
+                      "path, f32 products)", "ms_api": ms, "ms_graph": gms,
+            "tokens_per_s": 2048 / (gms / 1e3)}
 
 
 def run_extra(dev=None):

@@ -11,20 +11,28 @@
 // (K-major for the MMA), w_up [b] f32.  Accumulator D = h_tile . W^T lives in
 // TMEM (128 lanes = 128 tokens, N = b columns, f32).
 //
-// CTA roles (224 threads, one CTA per SM, persistent over row groups):
-//   warp 0      TMA producer: W k-chunk into the W ring, then one A k-chunk
-//               per tile into the A ring (128-row box, 32-row boxes for the
-//               ragged tail, or tile::gather4 rows when peeling by row_idx).
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer.  K-outer /
-//               M-inner: each W k-chunk in smem feeds up to 4 token tiles,
-//               whose accumulators all live in TMEM at once (4 x 128 cols),
-//               so W is re-read from L2 once per 512 tokens, not per 128.
-//   warps 2-5   sum-of-squares of every A slot from smem while the MMAs run
-//               (RMS statistics fused into the stream), then the epilogue:
-//               tcgen05.ld the row's b accumulators, scale, SiLU, dot w_up,
-//               f64 sigmoid, strict threshold, ballot the exit bits.
-//   warp 6      compaction: per-group popc scan + ordered decoupled look-back
-//               across groups, writes int64 exit / continuing indices.
+// CTA roles (352 threads, one CTA per SM, persistent over row groups of up
+// to 4 token tiles of 128 rows):
+//   warp 0      TMA producer: W k-chunks into the W ring, A k-chunks into the
+//               A ring (128-row boxes, 64/32/16-row boxes for the ragged
+//               tail, tile::gather4 rows when peeling by row_idx).
+//   warp 1      TMEM allocator + MMA issuer (one elected lane).  Phase 1,
+//               K-outer / M-inner: each W k-chunk in smem feeds every tile of
+//               the group, whose accumulators all live in TMEM (4 x 128 cols),
+//               so W is read from L2 once per group.  Phase 2, tile-major over
+//               the last nw k-chunks (their W slots stay resident): tiles
+//               complete one after another and their epilogues overlap the
+//               stream of later tiles.
+//   warps 2-9   two sets of 4 (set 0: tiles 0 and 2, set 1: tiles 1 and 3):
+//               sum of squares of their tiles' A slots from smem while the
+//               MMAs run (FHFMA), then each tile's epilogue as soon as its
+//               accumulator is complete: tcgen05.ld (two in flight), scale,
+//               SiLU (tanh form), dot w_up, f64 sigmoid, strict threshold,
+//               ballots.
+//   warp 10     compaction: per-group popc scan + flat look-back over all
+//               predecessors' tagged aggregates, int64 exit / continuing
+//               indices.
+// Launched with programmatic dependent launch (see route_tc_launch).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -137,7 +145,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if ((n32 + cpg - 1) / cpg > NG) NG = (n32 + cpg - 1) / cpg;
   const bool gathered = p.row_idx != nullptr;
   const bool need_scan = p.exit_idx || p.cont_idx || p.counts;
-  auto bounds = [&](int64_t g, int64_t& r0, int64_t& r1) { group_range(g, n, n32, NG, r0, r1); };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_w);
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     long long pw_cyc = 0, p_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      bounds(g, r0, r1);
+      group_range(g, n, n32, NG, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       if (gathered) {
         __syncwarp();
@@ -263,7 +270,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint64_t desc_hi = sw128_kmajor_desc(0);
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      bounds(g, r0, r1);
+      group_range(g, n, n32, NG, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
       tc_fence_after();
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     long long sw_cyc = 0, s_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      bounds(g, r0, r1);
+      group_range(g, n, n32, NG, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       // sum of squares of this thread's row for each of its two tiles
       // (t = wset, wset + 2), four f32 chains each, from the swizzled A slots
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int gi = 0;
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      bounds(g, r0, r1);
+      group_range(g, n, n32, NG, r0, r1);
       const int par = gi & 1;
       mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;

@@ -698,7 +698,7 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
     const char* w0 = reinterpret_cast<const char*>(w_ptrs[0]);
     for (int c = 1; c < C && stacked; ++c)
       stacked = reinterpret_cast<const char*>(w_ptrs[c]) == w0 + (size_t)c * b * d * 2;
-    static const char* tenv = getenv("TIDE_DECODE_TMA");
+    const char* tenv = getenv("TIDE_DECODE_TMA");
     if (stacked && !(tenv && tenv[0] == '0') &&
         make_map(&p.wmap, w_ptrs[0], dtype, d, (int64_t)C * b, d, 64, 128) == TIDE_OK)
       p.use_tma = 1;
@@ -708,7 +708,7 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
   static size_t attr[6] = {0, 0, 0, 0, 0, 0};
   // tensor-core path: slice CTAs of a checkpoint as one cluster (DSMEM
   // reduction) when S <= 16 and all C clusters fit; TIDE_DECODE_CLUSTER=0 disables
-  static const char* cenv = getenv("TIDE_DECODE_CLUSTER");
+  const char* cenv = getenv("TIDE_DECODE_CLUSTER");  // read per call (tests switch it)
   if (tc && !(cenv && cenv[0] == '0')) {
     // widest slice first (S = 16, then 8): fewer bytes per CTA, if co-resident
     for (int cw = cs; cw <= 4 * cs; cw *= 2) {

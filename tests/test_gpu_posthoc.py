@@ -256,3 +256,22 @@ def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch)
         assert np.all((got == want) | exc), tail
         out[tail] = got
     assert np.all((out["1"] == out["0"]) | exc)
+
+
+@pytest.mark.parametrize("variant", [{"TIDE_DECODE_CLUSTER": "0"}, {"TIDE_DECODE_TMA": "0"},
+                                     {"TIDE_DECODE_CLUSTER": "0", "TIDE_DECODE_TMA": "0"}])
+def test_decode_step_fallback_paths(variant, monkeypatch):
+    """The global-ticket reduction and the cp.async W path give the same exit
+    map as the default (cluster + TMA) decode kernel."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(36, 4096, 8, "bf16", 41, scale=0.3)
+    cfg = P.RuntimeConfig(exit_threshold=0.5)
+    want = P.select_exits(states, bank, cfg)
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    got = P.select_exits(states, bank, cfg)
+    scores, exc = {}, np.zeros(8, bool)
+    for k in ckpts:
+        s_, t, m = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
+        exc |= np.abs(t - O.logit_of(0.5)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
+    assert np.all((got.cpu().numpy() == want.cpu().numpy()) | exc)

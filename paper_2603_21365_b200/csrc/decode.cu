@@ -163,7 +163,7 @@ template <int NR>
 __device__ __forceinline__ void decode_tail(const DecParams& p, int c, int s, float* sRes, float* sWup,
                                             float* sLog, unsigned int* last_s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = (int)p.n, b = p.b;
+  const int b = p.b;
   const int tile = b * NR + NR;
   float* sSS = sRes + (size_t)b * NR;
   float* part = p.ws->partials;

@@ -67,30 +67,6 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void arrive_remote(uint32_t caddr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
-__device__ __forceinline__ void arrive_expect_remote(uint32_t caddr, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(caddr),
-               "r"(bytes)
-               : "memory");
-}
-// 2-CTA TMA: data lands in this CTA's smem, completion is counted on the
-// leader's barrier (cluster address).
-__device__ __forceinline__ void tma2_load_2d(void* dst, const CUtensorMap* m, uint32_t bar_c,
-                                             int c0, int c1, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::"
-      "cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(m), "r"(bar_c), "r"(c0), "r"(c1), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void tma2_gather4(void* dst, const CUtensorMap* m, uint32_t bar_c, int c0,
-                                             int r0, int r1, int r2, int r3, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::"
-      "complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(
-          smem_u32(dst)),
-      "l"(m), "r"(bar_c), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
-      : "memory");
-}
 __device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(dst_smem)),

@@ -102,14 +102,6 @@ __device__ __forceinline__ uint32_t dsmem_addr(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_dsmem_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-               "r"(d)
-               : "memory");
-}
 // bulk copy local smem -> smem of a CTA in the cluster, completing on its mbarrier
 __device__ __forceinline__ void bulk_s2dsmem(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
                                              uint32_t bar_cluster) {
@@ -118,10 +110,6 @@ __device__ __forceinline__ void bulk_s2dsmem(uint32_t dst_cluster, uint32_t src_
           dst_cluster),
       "r"(src_cta), "r"(bytes), "r"(bar_cluster)
       : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
 }
 // split arrive / wait: every CTA of the cluster has started (its shared
 // memory may be written remotely) once the wait returns

@@ -79,6 +79,109 @@ __device__ __forceinline__ void gemm_16x128(const XT* const* xrow, const XT* W, 
   }
 }
 
+// Vector path (rows and W 16-byte aligned, d and ld multiples of the vector
+// width): K chunks of kVK columns staged with 16-byte loads, the next chunk
+// prefetched into registers while the current one is multiplied, and the
+// inner product read from smem as float4 along k (32 FMAs per 6 LDS.128), so
+// the loop is FMA-bound instead of latency- / LDS-bound.
+constexpr int kVK = 64;            // K chunk of the vector path
+constexpr int kVP = kVK + 4;       // padded smem row (16-byte aligned, conflict-free float4 reads)
+constexpr size_t kVSmem = (size_t)(kSR + kSJ) * kVP * sizeof(float);
+
+template <typename XT> struct Vec16;  // 16 bytes of XT -> f32 lanes
+template <> struct Vec16<float> { static constexpr int N = 4; };
+template <> struct Vec16<__nv_bfloat16> { static constexpr int N = 8; };
+template <> struct Vec16<__half> { static constexpr int N = 8; };
+
+template <typename XT>
+__device__ __forceinline__ void gemm_16x128_vec(const XT* const* xrow, const XT* W, int64_t ldw,
+                                                int j0, int b, int64_t d, float (&acc)[2][4],
+                                                float* Xs, float* Ws, float* ss_s) {
+  constexpr int V = Vec16<XT>::N;
+  constexpr int XN = kSR * kVK / V, WN = kSJ * kVK / V;  // 16-byte pieces per chunk
+  constexpr int XPER = (XN + kSThreads - 1) / kSThreads;   // per thread
+  constexpr int WPER = (WN + kSThreads - 1) / kSThreads;
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  uint4 xr[XPER], wr[WPER];
+  auto load = [&](int64_t kc) {
+#pragma unroll
+    for (int u = 0; u < XPER; ++u) {
+      const int e = tid + u * kSThreads;
+      const int r = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      const int64_t k = kc + kk;
+      xr[u] = (e < XN && xrow[r] && k < d) ? ld_nc_v4(xrow[r] + k) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < WPER; ++u) {
+      const int e = tid + u * kSThreads;
+      const int j = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      const int64_t k = kc + kk;
+      wr[u] = (e < WN && j0 + j < b && k < d) ? ld_nc_v4(W + (int64_t)(j0 + j) * ldw + k)
+                                              : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int u = 0; u < XPER; ++u) {
+      const int e = tid + u * kSThreads;
+      if (e >= XN) break;
+      const int r = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      float f[V];
+      unpack16(xr[u], f, (const XT*)nullptr);
+#pragma unroll
+      for (int v = 0; v < V; ++v) Xs[r * kVP + kk + v] = f[v];
+    }
+#pragma unroll
+    for (int u = 0; u < WPER; ++u) {
+      const int e = tid + u * kSThreads;
+      if (e >= WN) break;
+      const int j = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      float f[V];
+      unpack16(wr[u], f, (const XT*)nullptr);
+#pragma unroll
+      for (int v = 0; v < V; ++v) Ws[j * kVP + kk + v] = f[v];
+    }
+  };
+  load(0);
+  for (int64_t kc = 0; kc < d; kc += kVK) {
+    store();
+    __syncthreads();
+    if (kc + kVK < d) load(kc + kVK);  // next chunk in flight during this one's math
+    if (ss_s && j0 == 0 && tid < kSR * 8) {
+      const int r = tid >> 3, part = tid & 7;
+      float sq = 0.f;
+#pragma unroll
+      for (int u = 0; u < kVK / 8; ++u) {
+        const float x = Xs[r * kVP + part * (kVK / 8) + u];
+        sq = fmaf(x, x, sq);
+      }
+      sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+      if (part == 0) ss_s[r] += sq;
+    }
+#pragma unroll 4
+    for (int kk = 0; kk < kVK; kk += 4) {
+      const float4 x0 = *reinterpret_cast<const float4*>(Xs + ty * kVP + kk);
+      const float4 x1 = *reinterpret_cast<const float4*>(Xs + (ty + 8) * kVP + kk);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 w = *reinterpret_cast<const float4*>(Ws + (tx + 32 * c) * kVP + kk);
+        acc[0][c] = fmaf(x0.x, w.x, acc[0][c]);
+        acc[0][c] = fmaf(x0.y, w.y, acc[0][c]);
+        acc[0][c] = fmaf(x0.z, w.z, acc[0][c]);
+        acc[0][c] = fmaf(x0.w, w.w, acc[0][c]);
+        acc[1][c] = fmaf(x1.x, w.x, acc[1][c]);
+        acc[1][c] = fmaf(x1.y, w.y, acc[1][c]);
+        acc[1][c] = fmaf(x1.z, w.z, acc[1][c]);
+        acc[1][c] = fmaf(x1.w, w.w, acc[1][c]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 struct SimtParams {
   int64_t n_host;
   const int64_t* n_dev;
@@ -101,10 +204,12 @@ struct SimtParams {
   Workspace* ws;
 };
 
-template <typename XT>
+template <typename XT, bool kVec>
 __global__ void __launch_bounds__(kSThreads) route_simt_kernel(const SimtParams p) {
-  __shared__ float Xs[kSR][kSK + 1];
-  __shared__ float Ws[kSJ][kSK + 1];
+  // scalar path: [kSR][kSK + 1] and [kSJ][kSK + 1]; vector path: rows of kVP
+  extern __shared__ float sm_f[];
+  float (*Xs)[kSK + 1] = reinterpret_cast<float (*)[kSK + 1]>(sm_f);
+  float (*Ws)[kSK + 1] = reinterpret_cast<float (*)[kSK + 1]>(sm_f + kSR * (kSK + 1));
   __shared__ float ss_s[kSR];
   __shared__ float t_s[kSR];
   __shared__ const XT* xrow[kSR];
@@ -127,7 +232,10 @@ __global__ void __launch_bounds__(kSThreads) route_simt_kernel(const SimtParams 
     __syncthreads();
     for (int j0 = 0; j0 < p.b; j0 += kSJ) {
       float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      gemm_16x128<XT>(xrow, W, p.d, j0, p.b, 0, p.d, acc, Xs, Ws, ss_s);
+      if (kVec)
+        gemm_16x128_vec<XT>(xrow, W, p.d, j0, p.b, p.d, acc, sm_f, sm_f + kSR * kVP, ss_s);
+      else
+        gemm_16x128<XT>(xrow, W, p.d, j0, p.b, 0, p.d, acc, Xs, Ws, ss_s);
       // all of ss_s is final after the first pass (j0 == 0) completed
 #pragma unroll
       for (int r2 = 0; r2 < 2; ++r2) {
@@ -217,10 +325,31 @@ int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
   const int64_t nblk = (a.n + kSR - 1) / kSR;
   if (nblk > kMaxParts / 2) return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)sm_count(dev) * 8));
+  // vector path when every 16-byte load is aligned
+  const int vw = a.dtype == TIDE_F32 ? 4 : 8;
+  const bool vec = a.d % vw == 0 && a.ld_h % vw == 0 &&
+                   ((reinterpret_cast<uintptr_t>(a.h) | reinterpret_cast<uintptr_t>(a.w_down)) & 15) == 0;
+  const size_t smem = vec ? kVSmem : (size_t)(kSR + kSJ) * (kSK + 1) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(route_simt_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVSmem);
+    cudaFuncSetAttribute(route_simt_kernel<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVSmem);
+    cudaFuncSetAttribute(route_simt_kernel<__half, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVSmem);
+    attr = true;
+  }
   switch (a.dtype) {
-    case TIDE_F32: route_simt_kernel<float><<<grid, kSThreads, 0, stream>>>(p); break;
-    case TIDE_BF16: route_simt_kernel<__nv_bfloat16><<<grid, kSThreads, 0, stream>>>(p); break;
-    case TIDE_F16: route_simt_kernel<__half><<<grid, kSThreads, 0, stream>>>(p); break;
+    case TIDE_F32:
+      if (vec) route_simt_kernel<float, true><<<grid, kSThreads, smem, stream>>>(p);
+      else route_simt_kernel<float, false><<<grid, kSThreads, smem, stream>>>(p);
+      break;
+    case TIDE_BF16:
+      if (vec) route_simt_kernel<__nv_bfloat16, true><<<grid, kSThreads, smem, stream>>>(p);
+      else route_simt_kernel<__nv_bfloat16, false><<<grid, kSThreads, smem, stream>>>(p);
+      break;
+    case TIDE_F16:
+      if (vec) route_simt_kernel<__half, true><<<grid, kSThreads, smem, stream>>>(p);
+      else route_simt_kernel<__half, false><<<grid, kSThreads, smem, stream>>>(p);
+      break;
     default: return set_error(TIDE_ERR_ARG, "bad dtype %d", a.dtype);
   }
   return check_launch("route_simt_kernel");

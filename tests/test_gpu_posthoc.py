@@ -236,7 +236,8 @@ def test_decode_step_object_matches_select_exits(mode):
 
 
 @pytest.mark.parametrize("d,n,L,scale,theta", [(4096, 4096, 32, 0.1, 0.5), (8192, 2048, 40, 0.06, 0.7),
-                                               (4096, 1000, 24, 0.2, 0.55)])
+                                               (4096, 1000, 24, 0.2, 0.55), (4096, 1000, 24, 0.2, 1.0),
+                                               (2048, 700, 28, 0.2, 0.6)])
 def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch):
     """The chain tail (one launch for the remaining checkpoints once few rows
     are live) gives the oracle's first-exit map (band rule), as the plain links do."""
@@ -256,6 +257,8 @@ def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch)
         assert np.all((got == want) | exc), tail
         out[tail] = got
     assert np.all((out["1"] == out["0"]) | exc)
+    if theta == 1.0:
+        assert np.all(out["1"] == P.NO_EXIT)
 
 
 @pytest.mark.parametrize("variant", [{"TIDE_DECODE_CLUSTER": "0"}, {"TIDE_DECODE_TMA": "0"},

@@ -164,7 +164,8 @@ int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_
  * score > theta in exit_layers[row id].  Only when *n_dev <= n_limit; else
  * nothing is routed.  *tail_count receives the live count the following
  * links must read (0 when the tail handled the rows, else *n_dev), so links
- * launched after it with n_dev = tail_count become no-ops.  scores: device
+ * launched after it with n_dev = tail_count become no-ops (or are skipped
+ * entirely inside a captured CUDA graph, see tide_capture_cond_*).  scores: device
  * scratch of C * cap f32 (cap = the chain's row capacity).  bf16 / f16.
  * (No reference counterpart: an execution strategy of posthoc_select.)
  */
@@ -173,7 +174,20 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
                     int64_t cap, int64_t n_limit, const void* const* w_ptrs,
                     const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
                     float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
-                    void* workspace, void* stream);
+                    uint64_t cond_handle, void* workspace, void* stream);
+
+/*
+ * CUDA-graph capture helpers for the links after a chain tail: during stream
+ * capture, tide_capture_cond_create makes a conditional handle (pass it as
+ * tide_route_tail's cond_handle: the tail's resolve step sets it to 0 when it
+ * handled the rows), tide_capture_cond_open adds an IF node on it after the
+ * captured work and returns a side stream capturing into the node's body (launch
+ * the remaining links there), tide_capture_cond_close ends that body.  Outside
+ * capture, cond_create returns handle 0 and the links run as plain launches.
+ */
+int tide_capture_cond_create(void* stream, uint64_t* handle);
+int tide_capture_cond_open(void* stream, uint64_t handle, void** body_stream);
+int tide_capture_cond_close(void* body_stream);
 
 #ifdef __cplusplus
 }

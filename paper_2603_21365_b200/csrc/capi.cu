@@ -130,7 +130,7 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
                     int64_t cap, int64_t n_limit, const void* const* w_ptrs,
                     const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
                     float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
-                    void* workspace, void* stream) {
+                    uint64_t cond_handle, void* workspace, void* stream) {
   if (C < 1 || !h_ptrs || !w_ptrs || !wup_ptrs || !layers)
     return set_error(TIDE_ERR_ARG, "tide_route_tail: bad checkpoint arrays");
   if (d < 1 || b < 1 || cap < 1 || ld_h < d || rows_total < 1 || n_limit < 0)
@@ -162,7 +162,64 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
   a.exit_layers = exit_layers;
   a.workspace = workspace;
   return route_tcs_tail_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, layers, n_limit, tail_count,
-                               reinterpret_cast<cudaStream_t>(stream));
+                               (unsigned long long)cond_handle, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// --- CUDA-graph conditional for the links after a chain tail -----------------
+int tide_capture_cond_create(void* stream, uint64_t* handle) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamGetCaptureInfo(s, &st, nullptr, &g, nullptr, nullptr) != cudaSuccess)
+    return set_error(TIDE_ERR_CUDA, "capture info failed");
+  if (st != cudaStreamCaptureStatusActive) {
+    *handle = 0;
+    return TIDE_OK;  // not capturing: nothing to do
+  }
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault) != cudaSuccess)
+    return set_error(TIDE_ERR_CUDA, "conditional handle");
+  *handle = (uint64_t)h;
+  return TIDE_OK;
+}
+
+int tide_capture_cond_open(void* stream, uint64_t handle, void** body_stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &deps, &nd) != cudaSuccess ||
+      st != cudaStreamCaptureStatusActive)
+    return set_error(TIDE_ERR_CUDA, "tide_capture_cond_open: stream not capturing");
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = (cudaGraphConditionalHandle)handle;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, deps, nd, &cp) != cudaSuccess)
+    return set_error(TIDE_ERR_CUDA, "conditional node");
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+    return set_error(TIDE_ERR_CUDA, "capture dependencies");
+  cudaStream_t side;
+  if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess)
+    return set_error(TIDE_ERR_CUDA, "side stream");
+  if (cudaStreamBeginCaptureToGraph(side, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
+      cudaSuccess)
+    return set_error(TIDE_ERR_CUDA, "capture to the conditional body");
+  *body_stream = side;
+  return TIDE_OK;
+}
+
+int tide_capture_cond_close(void* body_stream) {
+  cudaStream_t side = reinterpret_cast<cudaStream_t>(body_stream);
+  cudaGraph_t out = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(side, &out);
+  cudaStreamDestroy(side);
+  if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "end of the conditional body capture");
+  return TIDE_OK;
 }
 
 int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,

@@ -742,11 +742,15 @@ int tcs_launch(const RouteArgs& a, const SplitParams& p, const WMaps<NC>& wm, ui
 __global__ void chain_resolve_kernel(const float* scores, int64_t cap, int nc, TailLayers layers,
                                      float theta, const int64_t* n_dev, int64_t n_limit,
                                      const int64_t* row_idx, int64_t* exit_layers,
-                                     int64_t* tail_count) {
-  griddep_wait();
+                                     int64_t* tail_count, unsigned long long cond) {
   const int64_t n = *n_dev;
   const bool handled = n <= n_limit;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *tail_count = handled ? 0 : n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *tail_count = handled ? 0 : n;
+    // in a captured CUDA graph: the IF node holding the remaining links runs
+    // only when the tail did not handle the rows (tide_capture_cond_*)
+    if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, handled ? 0u : 1u);
+  }
   if (!handled) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -783,7 +787,7 @@ int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid) 
 int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                           const void* const* w_ptrs, const float* const* wup_ptrs,
                           const int64_t* layers, int64_t n_limit, int64_t* tail_count,
-                          cudaStream_t stream) {
+                          unsigned long long cond, cudaStream_t stream) {
   if (C < 1 || C > kMaxTailC) return set_error(TIDE_ERR_ARG, "tail: C must be in [1, %d]", kMaxTailC);
   if (!a.row_idx || !a.n_dev || !a.scores || !a.exit_layers || !tail_count)
     return set_error(TIDE_ERR_ARG, "tail: row_idx, n_dev, scores, exit_layers, tail_count required");
@@ -828,17 +832,11 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
     return rc;
   TailLayers tl{};
   for (int c = 0; c < C; ++c) tl.l[c] = layers[c];
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((n_limit + 255) / 256, 148)));
-  cfg.blockDim = dim3(256);
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, chain_resolve_kernel, (const float*)a.scores, (int64_t)a.n, C, tl, a.theta,
-                     a.n_dev, n_limit, a.row_idx, a.exit_layers, tail_count);
+  // plain launch (full dependency): a conditional graph node may follow it
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_limit + 255) / 256, 148));
+  chain_resolve_kernel<<<nb, 256, 0, stream>>>((const float*)a.scores, (int64_t)a.n, C, tl, a.theta,
+                                               a.n_dev, n_limit, a.row_idx, a.exit_layers,
+                                               tail_count, cond);
   return check_launch("chain_resolve_kernel");
 }
 

@@ -22,6 +22,7 @@ is this package's RouterBank or the reference's.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -251,18 +252,24 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
     # hold a handful of rows each, so per-link latency, not bytes, is their cost.
     tail_at = TAIL_AFTER - 1 if (code != N.F32 and len(ckpts) - TAIL_AFTER >= 2
                                  and _tail_enabled()) else -1
+    ls = s  # stream the links go to (a graph conditional's body after the tail)
+    body = None
     for i, k in enumerate(ckpts):
         wd, wu = device_weights(bank.routers[k], code, dev)
         h = staged[k + 1]
         N.check(lib.tide_route(h.data_ptr(), d, n, n_dev or None, n, d, code, row_idx or None,
                                wd.data_ptr(), wu.data_ptr(), b, eps, theta, k, None, None, None,
                                None, rem[i & 1].data_ptr(), 1, exit_layers.data_ptr(),
-                               cnt[i & 1].data_ptr(), ws, s), "tide_route")
+                               cnt[i & 1].data_ptr(), ws, ls), "tide_route")
         row_idx = rem[i & 1].data_ptr()
         n_dev = cnt[i & 1].data_ptr() + 8
         if i == tail_at:
-            n_dev = _chain_tail(lib, staged, bank, ckpts[i + 1:], code, dev, n, d, b, eps, theta,
-                                row_idx, n_dev, exit_layers, ws, s)
+            n_dev, body = _chain_tail(lib, staged, bank, ckpts[i + 1:], code, dev, n, d, b, eps,
+                                      theta, row_idx, n_dev, exit_layers, ws, s)
+            if body is not None:
+                ls = body.value
+    if body is not None:
+        N.check(lib.tide_capture_cond_close(body), "tide_capture_cond_close")
     return exit_layers
 
 
@@ -282,15 +289,25 @@ def _chain_tail(lib, staged, bank, rest, code, dev, n, d, b, eps, theta, row_idx
     wts = [device_weights(bank.routers[k], code, dev) for k in rest]
     scratch = torch.empty(len(rest) * n, dtype=torch.float32, device=dev)
     tail_count = torch.empty(1, dtype=torch.int64, device=dev)
+    # inside CUDA-graph capture the remaining links go into a conditional node
+    # that the tail switches off when it handled the rows (no idle launches)
+    cond = ctypes.c_uint64(0)
+    if torch.cuda.is_current_stream_capturing():
+        N.check(lib.tide_capture_cond_create(s, ctypes.byref(cond)), "tide_capture_cond_create")
     rc = lib.tide_route_tail(
         N.ptr_array([staged[k + 1].data_ptr() for k in rest]), len(rest), d, n, d, code, row_idx,
         n_dev, n, n_limit, N.ptr_array([w.data_ptr() for w, _ in wts]),
         N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(rest), eps, theta,
-        scratch.data_ptr(), exit_layers.data_ptr(), tail_count.data_ptr(), ws, s)
+        scratch.data_ptr(), exit_layers.data_ptr(), tail_count.data_ptr(), cond.value, ws, s)
     if rc:
-        return n_dev  # shape without a split-K plan: the links do the work
+        return n_dev, None  # shape without a split-K plan: the links do the work
     _chain_tail.keep = (scratch, tail_count)  # alive until the stream reaches them
-    return tail_count.data_ptr()
+    body = None
+    if cond.value:
+        body = ctypes.c_void_p()
+        N.check(lib.tide_capture_cond_open(s, cond.value, ctypes.byref(body)),
+                "tide_capture_cond_open")
+    return tail_count.data_ptr(), body
 
 
 class DecodeStep:

@@ -278,3 +278,35 @@ def test_decode_step_fallback_paths(variant, monkeypatch):
         s_, t, m = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
         exc |= np.abs(t - O.logit_of(0.5)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
     assert np.all((got.cpu().numpy() == want.cpu().numpy()) | exc)
+
+
+@pytest.mark.parametrize("d,n,L,scale,theta", [(4096, 4096, 32, 0.1, 0.5), (4096, 1000, 24, 0.2, 1.0),
+                                               (8192, 2048, 40, 0.06, 0.7)])
+def test_chain_captured_in_cuda_graph(d, n, L, scale, theta):
+    """select_exits captured in a CUDA graph (the links after the chain tail
+    sit in a conditional node the tail switches off) == eager, on replays with
+    new capture contents."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(L, d, n, "bf16", 90 + n, scale=scale)
+    cfg = P.RuntimeConfig(exit_threshold=theta)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        P.select_exits(states, bank, cfg)  # warm caches (weights, plans) outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            out = P.select_exits(states, bank, cfg)
+    torch.cuda.synchronize()
+    for rep in range(3):
+        if rep:
+            gen = torch.Generator(device="cuda")
+            gen.manual_seed(500 + rep)
+            for k in ckpts:
+                states[k + 1].copy_(torch.randn(states[k + 1].shape, generator=gen,
+                                                device="cuda").to(states[k + 1].dtype))
+            torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        want = P.select_exits(states, bank, cfg)
+        assert torch.equal(out, want), rep

@@ -38,7 +38,7 @@ struct LabelParams {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kLThreads) cos_label_kernel(const __grid_constant__ LabelParams p) {
+__global__ void __launch_bounds__(kLThreads, 2) cos_label_kernel(const __grid_constant__ LabelParams p) {
   constexpr int V = 16 / sizeof(T);
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kLThreads / 32);
@@ -60,17 +60,14 @@ __global__ void __launch_bounds__(kLThreads) cos_label_kernel(const __grid_const
       if (vec && sizeof(T) == 2) {
         // bf16 / f16: mixed-precision FMAs straight on the packed pairs
         constexpr bool kB = sizeof(T) == 2 && !std::is_same<T, __half>::value;
-        for (int k = lane * V; k < p.d; k += 32 * V) {
-          const uint4 fr = ld_nc_v4(f + k);
+        // two 16-byte steps per iteration: 18 loads in flight per lane (same
+        // per-lane element order as one step at a time -> identical sums)
+        auto step = [&](const uint4& fr, const uint4 (&raw)[kLBatch]) {
           const uint32_t fw[4] = {fr.x, fr.y, fr.z, fr.w};
           if (first) {
 #pragma unroll
             for (int w = 0; w < 4; ++w) dot2_acc<kB>(fw[w], fw[w], ssf);
           }
-          uint4 raw[kLBatch];
-#pragma unroll
-          for (int c = 0; c < kLBatch; ++c)
-            if (hp[c]) raw[c] = ld_nc_v4(hp[c] + k);
 #pragma unroll
           for (int c = 0; c < kLBatch; ++c) {
             if (hp[c]) {
@@ -82,6 +79,20 @@ __global__ void __launch_bounds__(kLThreads) cos_label_kernel(const __grid_const
               }
             }
           }
+        };
+        for (int k = lane * V; k < p.d; k += 64 * V) {
+          const int k2 = k + 32 * V;
+          const bool two = k2 < p.d;
+          const uint4 fr0 = ld_nc_v4(f + k);
+          const uint4 fr1 = two ? ld_nc_v4(f + k2) : make_uint4(0, 0, 0, 0);
+          uint4 raw0[kLBatch], raw1[kLBatch];
+#pragma unroll
+          for (int c = 0; c < kLBatch; ++c) {
+            raw0[c] = hp[c] ? ld_nc_v4(hp[c] + k) : make_uint4(0, 0, 0, 0);
+            raw1[c] = (hp[c] && two) ? ld_nc_v4(hp[c] + k2) : make_uint4(0, 0, 0, 0);
+          }
+          step(fr0, raw0);
+          if (two) step(fr1, raw1);
         }
       } else if (vec) {
         for (int k = lane * V; k < p.d; k += 32 * V) {

@@ -81,7 +81,27 @@ __global__ void __launch_bounds__(64 + 32 * NR, 1)
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0 && (p.flags & 128)) {
+      // quad order: W for 4 k-chunks, then per tile its 4 k-chunks back to back
+      // (the 4 boxes of a row's 512 contiguous bytes are requested together)
+      const uint64_t pol_h = policy_evict_first(), pol_w = policy_evict_last();
+      int as = 0, aph = 0, wsl = 0, wph = 0;
+      for (int kq = 0; kq < p.nk; kq += 4) {
+        for (int kc = kq; kc < kq + 4 && kc < p.nk; ++kc) {
+          mbar_wait(&w_empty[wsl], wph ^ 1);
+          mbar_arrive_expect_tx(&w_full[wsl], kSlot);
+          tma_load_2d(sW + wsl * kSlot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
+          if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
+        }
+        for (int t = 0; t < T; ++t)
+          for (int kc = kq; kc < kq + 4 && kc < p.nk; ++kc) {
+            mbar_wait(&a_empty[as], aph ^ 1);
+            mbar_arrive_expect_tx(&a_full[as], kSlot);
+            tma_load_2d(sA + as * kSlot, &tm_h, &a_full[as], kc * 64, r0 + 128 * t, pol_h);
+            if (++as == p.na) { as = 0; aph ^= 1; }
+          }
+      }
+    } else if (lane == 0) {
       const uint64_t pol_h = policy_evict_first(), pol_w = policy_evict_last();
       int as = 0, aph = 0, wsl = 0, wph = 0;
       for (int kc = 0; kc < p.nk; ++kc) {
@@ -357,10 +377,9 @@ int main(int argc, char** argv) {
     p.na = c.na;
     p.nw = c.nw;
     char nm[128];
-    for (uint32_t f : {7u, 71u, 39u}) {
-      if ((f & 32) && c.na % 2) continue;
+    for (uint32_t f : {4u, 132u, 7u, 135u}) {
       p.flags = f;
-      const char* fs = f == 7 ? "TMA+MMA+RMS" : f == 71 ? "TMA+MMA+RMS lastM64" : "TMA+MMA+RMS N256";
+      const char* fs = f == 4 ? "TMA" : f == 132 ? "TMA quad-order" : f == 7 ? "TMA+MMA+RMS" : "TMA+MMA+RMS quad";
       snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM0 NR8 RL0 (base)", c.na, c.nw, fs);
       show(nm, run<0, 8, 0>(th, tw, p, sms));
 

@@ -52,6 +52,8 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                           const int64_t* layers, int64_t n_limit, int64_t* tail_count,
                           unsigned long long cond, cudaStream_t stream);
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream);
+bool route_tf32_supported(int d, int b);
+int route_tf32_launch(const RouteArgs& a, cudaStream_t stream);
 int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
                    int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
                    int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,

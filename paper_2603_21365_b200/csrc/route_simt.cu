@@ -324,7 +324,6 @@ int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
   cudaGetDevice(&dev);
   const int64_t nblk = (a.n + kSR - 1) / kSR;
   if (nblk > kMaxParts / 2) return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)sm_count(dev) * 8));
   // vector path when every 16-byte load is aligned
   const int vw = a.dtype == TIDE_F32 ? 4 : 8;
   const bool vec = a.d % vw == 0 && a.ld_h % vw == 0 &&
@@ -337,21 +336,25 @@ int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
     cudaFuncSetAttribute(route_simt_kernel<__half, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVSmem);
     attr = true;
   }
+  void (*kern)(const SimtParams) = nullptr;
   switch (a.dtype) {
-    case TIDE_F32:
-      if (vec) route_simt_kernel<float, true><<<grid, kSThreads, smem, stream>>>(p);
-      else route_simt_kernel<float, false><<<grid, kSThreads, smem, stream>>>(p);
-      break;
+    case TIDE_F32: kern = vec ? route_simt_kernel<float, true> : route_simt_kernel<float, false>; break;
     case TIDE_BF16:
-      if (vec) route_simt_kernel<__nv_bfloat16, true><<<grid, kSThreads, smem, stream>>>(p);
-      else route_simt_kernel<__nv_bfloat16, false><<<grid, kSThreads, smem, stream>>>(p);
+      kern = vec ? route_simt_kernel<__nv_bfloat16, true> : route_simt_kernel<__nv_bfloat16, false>;
       break;
-    case TIDE_F16:
-      if (vec) route_simt_kernel<__half, true><<<grid, kSThreads, smem, stream>>>(p);
-      else route_simt_kernel<__half, false><<<grid, kSThreads, smem, stream>>>(p);
-      break;
+    case TIDE_F16: kern = vec ? route_simt_kernel<__half, true> : route_simt_kernel<__half, false>; break;
     default: return set_error(TIDE_ERR_ARG, "bad dtype %d", a.dtype);
   }
+  // CTAs walk blocks blk, blk + grid, ... and each block's look-back waits on
+  // every lower block: the grid must be fully co-resident, or a CTA spinning
+  // on its second block waits for a first block whose CTA cannot be scheduled
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSThreads, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(nblk, (int64_t)sm_count(dev) * std::min(per_sm, 8)));
+  kern<<<grid, kSThreads, smem, stream>>>(p);
   return check_launch("route_simt_kernel");
 }
 

@@ -609,10 +609,11 @@ int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, int64_t 
   EncodeTiledFn enc = encode_fn();
   if (!enc) return set_error(TIDE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t gstride[1] = {(cuuint64_t)ld_elems * 2};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ld_elems * (dtype == TIDE_F32 ? 4 : 2)};
   const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t estride[2] = {1, 1};
-  CUresult r = enc(m, dtype == TIDE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+  CUresult r = enc(m, dtype == TIDE_BF16  ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                     : dtype == TIDE_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    2, const_cast<void*>(base), gdim, gstride, box, estride,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

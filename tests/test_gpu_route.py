@@ -300,3 +300,44 @@ def test_headline_shape_full_size():
     e, c = O.compact_indices(mask)
     np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
     np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("n,d", [(20000, 256), (70000, 128)])
+def test_f32_many_blocks_with_compaction(n, d):
+    """CUDA-core f32 kernel with more 16-row blocks than co-resident CTAs and
+    the look-back on (regression: a grid larger than what fits on the SMs
+    deadlocked the look-back)."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(n + d))
+    b = 128
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = g.standard_normal((n, d), dtype=np.float32)
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, "f32"), _router(wd, wu), theta=0.5, want_logits=True,
+                want_indices=True)
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, "f32", f"n={n}")
+    e, c = O.compact_indices(r["mask"].cpu().numpy())
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("n,d,b", [(2048, 768, 128), (1000, 772, 96), (300, 100, 40),
+                                   (9000, 256, 128)])
+def test_f32_tensor_core_opt_in(n, d, b, monkeypatch):
+    """Opt-in 3xTF32 tcgen05 kernel (TIDE_F32_TC=1, route_tf32.cu) inside the
+    f32 contract at GPT-2-small widths; compaction bit-exact."""
+    need_gpu()
+    monkeypatch.setenv("TIDE_F32_TC", "1")
+    assert N.load().tide_route_uses_tensor_cores(N.F32, d, b) == 1
+    g = np.random.Generator(np.random.PCG64(3 * n + d + b))
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = g.standard_normal((n, d), dtype=np.float32) * 3.0
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, "f32"), _router(wd, wu), theta=0.5, want_logits=True,
+                want_indices=True)
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, "f32", f"tf32 n={n} d={d}")
+    e, c = O.compact_indices(r["mask"].cpu().numpy())
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)

@@ -153,11 +153,30 @@ def config1():
             "tokens_per_s": 2048 / (gms / 1e3)}
 
 
+def training(n=65_536, d=4096, epochs=2):
+    """GPU router training (§8f-4) on one checkpoint's calibration rows."""
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(6)
+    x = torch.randn((n, d), generator=gen, device="cuda")
+    y = (x[:, 0] > 0).to(torch.float32)
+    cfg = P.CalibrationConfig(epochs=epochs, batch_size=1024, learning_rate=1e-3)
+    P.train_router(x[:4096], y[:4096], 3, P.CalibrationConfig(epochs=1))  # warm-up
+    torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    _, st = P.train_router(x, y, 3, cfg)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    return {"config": f"router training (GPU), {n:,} rows x d={d}, b=128, batch 1024, "
+                      f"{epochs} epochs", "s_total": sec, "ms_per_epoch": sec / epochs * 1e3,
+            "rows_per_s": n * epochs / sec, "accuracy": st.accuracy}
+
+
 def run_extra(dev=None):
     out = []
     for fn in (config1, config2, config3,
                lambda: config3(P.BATCH_UNANIMOUS), lambda: config3(dtype=torch.float16),
-               config5, config4):
+               config5, config4, training):
         try:
             out.append(fn())
         except Exception as e:  # report, do not hide

@@ -139,6 +139,29 @@ int tide_cos_label(const void* const* ckpt_ptrs, int32_t C, const void* final_h,
                    int64_t* zero_counts, void* stream);
 
 /*
+ * Router training, one minibatch (ee/calibration.py:238-290; host side in
+ * training.py, whose GEMMs are library calls).  Per row i of u [rows, b] f32
+ * (= z_batch W_down^T):  su = sigma(u), a = u*su, t = a . w_up,
+ *   gt[i] = (sigma(t) - labels[i]) / rows,  gu = gt * w_up * su*(1 + u*(1 - su)),
+ *   *loss_sum += max(t,0) - t*y + log1p(exp(-|t|))   (f64 accumulator).
+ * Outputs a_out / gu_out [rows, b], gt_out / t_out [rows], loss_sum: any may
+ * be NULL.
+ */
+int tide_train_act(const float* u, int64_t rows, int32_t b, const float* w_up,
+                   const float* labels, float* a_out, float* gu_out, float* gt_out,
+                   float* t_out, double* loss_sum, void* stream);
+
+/*
+ * One Adam step over count f32 elements (ee/calibration.py:277-290), the
+ * reference's rounding order: m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g;
+ * w -= lr * (m / bias_corr1) / (sqrt(v / bias_corr2) + eps), with
+ * bias_corr_k = f32(1 - beta_k^t) computed by the caller.
+ */
+int tide_adam_step(float* w, const float* g, float* m, float* v, int64_t count, float beta1,
+                   float one_minus_beta1, float beta2, float one_minus_beta2, float bias_corr1,
+                   float bias_corr2, float lr, float eps, void* stream);
+
+/*
  * Decode-step router (n <= TIDE_MAX_DECODE_ROWS rows, every checkpoint in ONE
  * launch) + exit resolution of posthoc_select (ee/runtime.py:151-178):
  * per-token = first checkpoint >= k_min whose score > theta; batch-unanimous

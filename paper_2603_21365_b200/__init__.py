@@ -18,6 +18,7 @@ from .router_ops import (SMALL_BATCH_CUTOVER, CompactionResult, Router, batch_co
 from .runtime import (BATCH_UNANIMOUS, FINAL_KEY, MODES, NO_EXIT, PER_TOKEN, DecodeStep,
                       OutputHead, PhaseStats, RuntimeConfig, posthoc_select, select_exits)
 from .tensor_math import DEFAULT_EPS, batched_cosine_similarity
+from .training import TrainingDivergedError, train_router
 
 __version__ = "0.1.0"
 
@@ -29,7 +30,8 @@ __all__ = [
     "BATCH_UNANIMOUS", "FINAL_KEY", "MODES", "NO_EXIT", "PER_TOKEN", "DecodeStep", "OutputHead",
     "PhaseStats",
     "RuntimeConfig", "posthoc_select", "select_exits",
-    "DEFAULT_EPS", "batched_cosine_similarity", "__version__",
+    "DEFAULT_EPS", "batched_cosine_similarity", "__version__", "train_router",
+    "TrainingDivergedError",
     "load_bank", "save_bank", "bank_file_size", "install_device_weights", "BinaryFormatError",
     "BadMagicError", "VersionError", "TruncatedError", "ChecksumError", "DimensionError",
 ]

@@ -3,9 +3,10 @@
 The bank / checkpoint objects keep the reference's fields and validation, so
 a reference `earlyexit.RouterBank` and this one are interchangeable inputs to
 `posthoc_select`.  `compute_labels` runs the one-pass cosine labeller kernel
-over every checkpoint at once.  Hidden-state collection (it needs the
-reference's stand-in transformer) and router training are out of scope
-(SURVEY.md §2 rows 11-12).
+over every checkpoint at once.  Router training runs on the GPU in
+training.py; hidden-state collection through the
+reference's stand-in transformer is out of scope (the CheckpointCapture hook
+collects from a real model instead).
 """
 
 from __future__ import annotations

@@ -1,0 +1,131 @@
+"""GPU router training (training.py, csrc/train.cu) against
+the real reference's train_router (tests/golden/train.npz, written by
+tests/golden/make_train_golden.py) and the reference's own TestTrainRouter
+cases (pkg/tests/test_calibration.py:236-296, test_acceptance.py:117-130)."""
+
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_21365_b200 as P
+from paper_2603_21365_b200 import training as T
+from tests.conftest import GOLDEN
+from tests.golden.make_train_golden import TRAIN_CASES, case_data
+from tests.gpu_helpers import need_gpu
+
+
+@pytest.fixture(scope="module")
+def golden_train():
+    return np.load(os.path.join(GOLDEN, "train.npz"))
+
+
+def test_empty_dataset_rejected():
+    with pytest.raises(ValueError, match="empty"):
+        T.train_router(np.zeros((0, 8), np.float32), np.zeros(0, np.float32), 3,
+                       P.CalibrationConfig())
+
+
+def test_label_shape_rejected():
+    with pytest.raises(ValueError, match="labels shape"):
+        T.train_router(np.zeros((4, 8), np.float32), np.zeros(5, np.float32), 3,
+                       P.CalibrationConfig())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(TRAIN_CASES))
+def test_matches_reference_training(golden_train, name):
+    """Same init, minibatch order and update rule as the reference: weights and
+    stats agree to the f32 rounding of the GEMM summation order."""
+    need_gpu()
+    x, y = case_data(name)
+    kw = TRAIN_CASES[name][5]
+    r, st = T.train_router(x, y, 3, P.CalibrationConfig(**kw))
+    wd_ref = golden_train[f"{name}__w_down"]
+    wu_ref = golden_train[f"{name}__w_up"]
+    ex, pos, loss, acc, flags = golden_train[f"{name}__stats"]
+    assert r.w_down.shape == wd_ref.shape and r.w_up.shape == wu_ref.shape
+    assert (st.examples, st.positives, st.flags) == (int(ex), int(pos), int(flags))
+    e_down = np.max(np.abs(r.w_down - wd_ref)) / np.max(np.abs(wd_ref))
+    e_up = np.max(np.abs(r.w_up - wu_ref)) / np.max(np.abs(wu_ref))
+    print(f"{name}: w_down rel {e_down:.2e} w_up rel {e_up:.2e} loss {st.final_loss:.6f} "
+          f"vs {loss:.6f} acc {st.accuracy} vs {acc}")
+    # measured on B200: <= 7.7e-6 (weights), loss to 6 digits
+    assert e_down <= 1e-4 and e_up <= 1e-4, (e_down, e_up)
+    assert st.final_loss == pytest.approx(loss, rel=1e-5, abs=1e-7)
+    assert abs(st.accuracy - acc) <= 2.0 / st.examples
+
+
+@pytest.mark.gpu
+def test_linearly_separable_reaches_high_accuracy():
+    need_gpu()
+    x, y = case_data("separable_d64")
+    _, st = T.train_router(x, y, 3, P.CalibrationConfig(**TRAIN_CASES["separable_d64"][5]))
+    assert st.accuracy >= 0.98 and st.examples == 2000 and not st.flags
+
+
+@pytest.mark.gpu
+def test_trainability_budget():
+    """Acceptance #4 (test_acceptance.py:117-130): 5,000 x 64, 100 epochs."""
+    need_gpu()
+    rng = np.random.Generator(np.random.PCG64(404))
+    x = rng.standard_normal((5_000, 64), dtype=np.float32)
+    x[:, 0] *= 4.0
+    y = (x[:, 0] > 0).astype(np.float32)
+    t0 = time.perf_counter()
+    _, st = T.train_router(x, y, 3, P.CalibrationConfig(epochs=100, learning_rate=1e-3, seed=7))
+    assert st.accuracy >= 0.99
+    assert time.perf_counter() - t0 < 20.0
+
+
+@pytest.mark.gpu
+def test_single_class_dataset():
+    need_gpu()
+    rng = np.random.Generator(np.random.PCG64(8))
+    x = rng.standard_normal((500, 32), dtype=np.float32)
+    _, st = T.train_router(x, np.ones(500, np.float32), 3,
+                           P.CalibrationConfig(epochs=100, learning_rate=1e-2, batch_size=256))
+    assert st.accuracy == 1.0 and st.flags & P.calibration.FLAG_SINGLE_CLASS
+    assert st.positives == 500
+
+
+@pytest.mark.gpu
+def test_deterministic_and_layer_seeded():
+    need_gpu()
+    rng = np.random.Generator(np.random.PCG64(12))
+    x = rng.standard_normal((300, 16), dtype=np.float32)
+    y = (x[:, 1] > 0).astype(np.float32)
+    cfg = P.CalibrationConfig(epochs=5, seed=9)
+    r1, s1 = T.train_router(x, y, 3, cfg)
+    r2, s2 = T.train_router(x, y, 3, cfg)
+    assert np.array_equal(r1.w_down, r2.w_down) and np.array_equal(r1.w_up, r2.w_up)
+    assert s1 == s2
+    r7, _ = T.train_router(x, y, 7, cfg)
+    assert not np.array_equal(r1.w_down, r7.w_down)
+
+
+@pytest.mark.gpu
+def test_divergence_detected():
+    need_gpu()
+    rng = np.random.Generator(np.random.PCG64(13))
+    x = rng.standard_normal((64, 8), dtype=np.float32)
+    y = (x[:, 0] > 0).astype(np.float32)
+    with pytest.raises(T.TrainingDivergedError, match="layer 3"):
+        T.train_router(x, y, 3, P.CalibrationConfig(learning_rate=1e30, epochs=3))
+
+
+@pytest.mark.gpu
+def test_bottleneck_and_device_features():
+    """bottleneck override; a CUDA-tensor dataset (collected on the device)
+    trains to the same router as its host copy."""
+    need_gpu()
+    rng = np.random.Generator(np.random.PCG64(14))
+    x = rng.standard_normal((700, 64), dtype=np.float32)
+    y = (x[:, 3] > 0).astype(np.float32)
+    cfg = P.CalibrationConfig(epochs=2, bottleneck=8, batch_size=200)
+    r_host, s_host = T.train_router(x, y, 3, cfg)
+    assert r_host.w_down.shape == (8, 64)
+    r_dev, s_dev = T.train_router(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), 3, cfg)
+    assert np.array_equal(r_host.w_down, r_dev.w_down) and s_host == s_dev

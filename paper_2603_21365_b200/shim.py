@@ -47,6 +47,25 @@ _PATCHES = [
 _saved: dict = {}
 
 
+def _train_router_for(earlyexit_pkg):
+    """GPU train_router returning the reference's own Router / RouterStats and
+    raising its TrainingDivergedError (ee/calibration.py:40-41,264-274)."""
+    from . import training as _tr
+    ref_cal = earlyexit_pkg.calibration
+    ref_ops = earlyexit_pkg.router_ops
+
+    def train_router(features, labels, layer, config):
+        try:
+            r, st = _tr.train_router(features, labels, layer, config)
+        except _tr.TrainingDivergedError as e:
+            raise ref_cal.TrainingDivergedError(str(e)) from e
+        return (ref_ops.Router(layer=r.layer, w_down=r.w_down, w_up=r.w_up),
+                ref_cal.RouterStats(examples=st.examples, positives=st.positives,
+                                    final_loss=st.final_loss, accuracy=st.accuracy,
+                                    flags=st.flags))
+    return train_router
+
+
 def _resolve(root, path):
     obj = root
     parts = path.split(".")
@@ -61,7 +80,9 @@ def install(earlyexit_pkg) -> list:
     for sub in ("router_ops", "runtime", "tensor_math", "calibration"):
         importlib.import_module(f"{earlyexit_pkg.__name__}.{sub}")
     done = []
-    for path, fn in _PATCHES:
+    trainer = _train_router_for(earlyexit_pkg)
+    patches = _PATCHES + [("calibration.train_router", trainer), ("train_router", trainer)]
+    for path, fn in patches:
         try:
             owner, name = _resolve(earlyexit_pkg, path)
         except AttributeError:
@@ -74,7 +95,7 @@ def install(earlyexit_pkg) -> list:
 
 
 def uninstall(earlyexit_pkg) -> None:
-    for path, _ in _PATCHES:
+    for path in [p for p, _ in _PATCHES] + ["calibration.train_router", "train_router"]:
         key = (id(earlyexit_pkg), path)
         if key in _saved:
             owner, name = _resolve(earlyexit_pkg, path)

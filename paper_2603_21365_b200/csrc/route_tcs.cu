@@ -797,8 +797,14 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
   const int nk = (a.d + 63) / 64;
   const int per = std::max(1, sm_count(dev) / C);
   int ks = 1;
+  // Cluster size cap 2 (TIDE_TAIL_KS overrides): the tail's rows are few but
+  // its checkpoints many, so more clusters per checkpoint, each streaming a
+  // longer K range, beat wide splits (tools/tail_sweep.py: config 2
+  // 0.109 -> 0.093 ms, config 5 0.252 -> 0.183 ms against a cap of 16).
+  const char* kenv = getenv("TIDE_TAIL_KS");
+  const int kcap = kenv ? atoi(kenv) : 2;
   for (int c = 16; c >= 2; c >>= 1)
-    if (c <= per && c <= nk && L0.bp % (8 * c) == 0 &&
+    if (c <= kcap && c <= per && c <= nk && L0.bp % (8 * c) == 0 &&
         tcs_max_clusters(dev, c, L0.smem_bytes) * c >= (per / c) * c * 1) {
       ks = c;
       break;

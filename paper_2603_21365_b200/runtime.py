@@ -250,8 +250,9 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
     # every remaining checkpoint in ONE launch (when few enough: n_limit) and
     # the remaining links become no-ops — the later links of a peeling chain
     # hold a handful of rows each, so per-link latency, not bytes, is their cost.
-    tail_at = TAIL_AFTER - 1 if (code != N.F32 and len(ckpts) - TAIL_AFTER >= 2
-                                 and _tail_enabled()) else -1
+    after = _tail_after()
+    tail_at = after - 1 if (code != N.F32 and len(ckpts) - after >= 2
+                            and _tail_enabled()) else -1
     ls = s  # stream the links go to (a graph conditional's body after the tail)
     body = None
     for i, k in enumerate(ckpts):
@@ -281,11 +282,17 @@ def _tail_enabled() -> bool:
     return os.environ.get("TIDE_CHAIN_TAIL", "1") != "0"
 
 
+def _tail_after() -> int:
+    import os
+    return int(os.environ.get("TIDE_TAIL_AFTER", TAIL_AFTER))
+
+
 def _chain_tail(lib, staged, bank, rest, code, dev, n, d, b, eps, theta, row_idx, n_dev,
                 exit_layers, ws, s):
     """tide_route_tail over the remaining checkpoints; returns the live-count
     pointer the following links read (0 rows when the tail handled them)."""
-    n_limit = int(min(n, max(128, (2048 * 4096) // d)))
+    import os
+    n_limit = int(min(n, max(128, int(os.environ.get("TIDE_TAIL_ROWS", 2048)) * 4096 // d)))
     wts = [device_weights(bank.routers[k], code, dev) for k in rest]
     scratch = torch.empty(len(rest) * n, dtype=torch.float32, device=dev)
     tail_count = torch.empty(1, dtype=torch.int64, device=dev)

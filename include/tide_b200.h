@@ -155,11 +155,15 @@ int tide_train_act(const float* u, int64_t rows, int32_t b, const float* w_up,
  * One Adam step over count f32 elements (ee/calibration.py:277-290), the
  * reference's rounding order: m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g;
  * w -= lr * (m / bias_corr1) / (sqrt(v / bias_corr2) + eps), with
- * bias_corr_k = f32(1 - beta_k^t) computed by the caller.
+ * bias_corr_k = f32(1 - beta_k^t) computed by the caller: the two scalars,
+ * or (bias_corr_table != NULL, for a captured CUDA graph replayed every
+ * epoch) the pair table[2 t], table[2 t + 1] at t = *step_base + step_offset
+ * (device memory).
  */
 int tide_adam_step(float* w, const float* g, float* m, float* v, int64_t count, float beta1,
-                   float one_minus_beta1, float beta2, float one_minus_beta2, float bias_corr1,
-                   float bias_corr2, float lr, float eps, void* stream);
+                   float one_minus_beta1, float beta2, float one_minus_beta2,
+                   const float* bias_corr_table, const int64_t* step_base, int64_t step_offset,
+                   float bias_corr1, float bias_corr2, float lr, float eps, void* stream);
 
 /*
  * Decode-step router (n <= TIDE_MAX_DECODE_ROWS rows, every checkpoint in ONE

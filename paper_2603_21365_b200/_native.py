@@ -54,7 +54,7 @@ SIGNATURES = {
     "tide_train_act": (ctypes.c_int, [_c_p, _i64, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                       _c_p, _c_p]),
     "tide_adam_step": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _f32, _f32, _f32, _f32,
-                                      _f32, _f32, _f32, _f32, _c_p]),
+                                      _c_p, _c_p, _i64, _f32, _f32, _f32, _f32, _c_p]),
     "tide_route_decode": (ctypes.c_int, [ctypes.POINTER(_c_p), _i32, _i64, _i64, _i32, _i32,
                                          ctypes.POINTER(_c_p), ctypes.POINTER(_c_p), _i32,
                                          ctypes.POINTER(_i64), _f32, _f32, _i64, _i32, _c_p,

@@ -64,8 +64,14 @@ __global__ void __launch_bounds__(32 * kTrainWarps)
 
 __global__ void adam_kernel(float* __restrict__ w, const float* __restrict__ g,
                             float* __restrict__ m, float* __restrict__ v, int64_t count, float b1,
-                            float c1, float b2, float c2, float bc1, float bc2, float lr,
-                            float eps) {
+                            float c1, float b2, float c2, const float* __restrict__ bc_table,
+                            const int64_t* __restrict__ step_base, int64_t step_offset,
+                            float bc1, float bc2, float lr, float eps) {
+  if (bc_table) {  // step-dependent bias corrections from device memory (graph replay)
+    const int64_t t = *step_base + step_offset;
+    bc1 = bc_table[2 * t];
+    bc2 = bc_table[2 * t + 1];
+  }
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
        k += (int64_t)gridDim.x * blockDim.x) {
     const float gk = g[k];
@@ -98,9 +104,12 @@ extern "C" int tide_train_act(const float* u, int64_t rows, int32_t b, const flo
 
 extern "C" int tide_adam_step(float* w, const float* g, float* m, float* v, int64_t count,
                               float beta1, float one_minus_beta1, float beta2,
-                              float one_minus_beta2, float bias_corr1, float bias_corr2, float lr,
-                              float eps, void* stream) {
+                              float one_minus_beta2, const float* bias_corr_table,
+                              const int64_t* step_base, int64_t step_offset, float bias_corr1,
+                              float bias_corr2, float lr, float eps, void* stream) {
   if (count < 0) return set_error(TIDE_ERR_ARG, "tide_adam_step: bad count");
+  if (bias_corr_table && !step_base)
+    return set_error(TIDE_ERR_ARG, "tide_adam_step: bias_corr_table needs step_base");
   if (count > 0 && (!w || !g || !m || !v))
     return set_error(TIDE_ERR_ARG, "tide_adam_step: null buffer");
   if (count == 0) return TIDE_OK;
@@ -108,8 +117,8 @@ extern "C" int tide_adam_step(float* w, const float* g, float* m, float* v, int6
   cudaGetDevice(&dev);
   const int64_t want = (count + 255) / 256;
   const int grid = (int)std::min<int64_t>(want, (int64_t)sm_count(dev) * 8);
-  adam_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(w, g, m, v, count, beta1, one_minus_beta1,
-                                                       beta2, one_minus_beta2, bias_corr1,
-                                                       bias_corr2, lr, eps);
+  adam_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      w, g, m, v, count, beta1, one_minus_beta1, beta2, one_minus_beta2, bias_corr_table,
+      step_base, step_offset, bias_corr1, bias_corr2, lr, eps);
   return check_launch("adam_kernel");
 }

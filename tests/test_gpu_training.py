@@ -129,3 +129,17 @@ def test_bottleneck_and_device_features():
     assert r_host.w_down.shape == (8, 64)
     r_dev, s_dev = T.train_router(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), 3, cfg)
     assert np.array_equal(r_host.w_down, r_dev.w_down) and s_host == s_dev
+
+
+@pytest.mark.gpu
+def test_graph_replay_equals_eager(monkeypatch):
+    """Epochs replayed from one captured graph == every launch issued eagerly."""
+    need_gpu()
+    x, y = case_data("ragged_batches_d96")
+    cfg = P.CalibrationConfig(**TRAIN_CASES["ragged_batches_d96"][5])
+    monkeypatch.setenv("TIDE_TRAIN_GRAPH", "1")
+    r_g, s_g = T.train_router(x, y, 3, cfg)
+    monkeypatch.setenv("TIDE_TRAIN_GRAPH", "0")
+    r_e, s_e = T.train_router(x, y, 3, cfg)
+    assert np.array_equal(r_g.w_down, r_e.w_down) and np.array_equal(r_g.w_up, r_e.w_up)
+    assert s_g == s_e

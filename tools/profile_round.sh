@@ -10,6 +10,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
     --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-check > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:route_tc -s 3 -c 1 \
     -o gpurun_out/prof_${TAG}_route_tc python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-check > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"cos_label|decode_tc|route_tcs|select_project|compact_kernel|route_simt" -c 16 \
+ncu --set full --clock-control none --import-source on -k regex:"cos_label|decode_tc|route_tcs|select_project|compact_kernel|route_simt|train_act|adam_kernel|route_tf32|chain_resolve" -c 48 \
     -o gpurun_out/prof_${TAG}_aux python tools/profile_aux.py > /dev/null 2>&1
 ls -la gpurun_out/

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -295,6 +296,200 @@ __global__ void __launch_bounds__(kSThreads) route_simt_kernel(const SimtParams 
   if (tid == 0) launch_done(p.ws);
 }
 
+// Wide variant for many rows (vector path only): 64 rows per CTA, each thread
+// 8 rows x 4 bottleneck columns (warp w: rows w, w+8, ..., so the X operand
+// is a broadcast read), 128 FMAs per 12 LDS.128 instead of 32 per 6 — the
+// 16-row kernel is shared-memory-bound, this one is FMA-bound.  Same
+// numerics per output (f32 products, k order).
+constexpr int kWR = 64;
+constexpr int kWRT = kWR / 8;  // rows per thread
+constexpr size_t kWSmem = (size_t)(kWR + kSJ) * kVP * sizeof(float);
+
+template <typename XT>
+__device__ __forceinline__ void gemm_wide(const XT* const* xrow, const XT* W, int64_t ldw, int j0,
+                                          int b, int64_t d, float (&acc)[kWRT][4], float* Xs,
+                                          float* Ws, float* ss_s) {
+  constexpr int V = Vec16<XT>::N;
+  constexpr int XN = kWR * kVK / V, WN = kSJ * kVK / V;
+  constexpr int XPER = XN / kSThreads, WPER = WN / kSThreads;
+  static_assert(XN % kSThreads == 0 && WN % kSThreads == 0, "tile pieces");
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  uint4 xr[XPER], wr[WPER];
+  auto load = [&](int64_t kc) {
+#pragma unroll
+    for (int u = 0; u < XPER; ++u) {
+      const int e = tid + u * kSThreads;
+      const int r = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      const int64_t k = kc + kk;
+      xr[u] = (xrow[r] && k < d) ? ld_nc_v4(xrow[r] + k) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < WPER; ++u) {
+      const int e = tid + u * kSThreads;
+      const int j = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      const int64_t k = kc + kk;
+      wr[u] = (j0 + j < b && k < d) ? ld_nc_v4(W + (int64_t)(j0 + j) * ldw + k)
+                                    : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int u = 0; u < XPER; ++u) {
+      const int e = tid + u * kSThreads;
+      const int r = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      float f[V];
+      unpack16(xr[u], f, (const XT*)nullptr);
+#pragma unroll
+      for (int v = 0; v < V; ++v) Xs[r * kVP + kk + v] = f[v];
+    }
+#pragma unroll
+    for (int u = 0; u < WPER; ++u) {
+      const int e = tid + u * kSThreads;
+      const int j = e / (kVK / V), kk = (e % (kVK / V)) * V;
+      float f[V];
+      unpack16(wr[u], f, (const XT*)nullptr);
+#pragma unroll
+      for (int v = 0; v < V; ++v) Ws[j * kVP + kk + v] = f[v];
+    }
+  };
+  load(0);
+  for (int64_t kc = 0; kc < d; kc += kVK) {
+    store();
+    __syncthreads();
+    if (kc + kVK < d) load(kc + kVK);
+    if (ss_s && j0 == 0) {
+#pragma unroll
+      for (int e = tid; e < kWR * 8; e += kSThreads) {
+        const int r = e >> 3, part = e & 7;
+        float sq = 0.f;
+#pragma unroll
+        for (int u = 0; u < kVK / 8; ++u) {
+          const float x = Xs[r * kVP + part * (kVK / 8) + u];
+          sq = fmaf(x, x, sq);
+        }
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+        if (part == 0) ss_s[r] += sq;
+      }
+    }
+#pragma unroll 2
+    for (int kk = 0; kk < kVK; kk += 4) {
+      float4 w[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) w[c] = *reinterpret_cast<const float4*>(Ws + (tx + 32 * c) * kVP + kk);
+#pragma unroll
+      for (int i = 0; i < kWRT; ++i) {
+        const float4 x = *reinterpret_cast<const float4*>(Xs + (ty + 8 * i) * kVP + kk);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[i][c] = fmaf(x.x, w[c].x, acc[i][c]);
+          acc[i][c] = fmaf(x.y, w[c].y, acc[i][c]);
+          acc[i][c] = fmaf(x.z, w[c].z, acc[i][c]);
+          acc[i][c] = fmaf(x.w, w[c].w, acc[i][c]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(kSThreads, 1) route_simt_wide_kernel(const SimtParams p) {
+  extern __shared__ float sm_f[];
+  __shared__ float ss_s[kWR];
+  __shared__ float t_s[kWR];
+  __shared__ const XT* xrow[kWR];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
+  const uint32_t tag = launch_tag(p.ws);
+  const int64_t nblk = (n + kWR - 1) / kWR;
+  const XT* h = reinterpret_cast<const XT*>(p.h);
+  const XT* W = reinterpret_cast<const XT*>(p.w_down);
+  const bool gathered = p.row_idx != nullptr;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t r0 = blk * kWR;
+    if (tid < kWR) {
+      const int64_t r = r0 + tid;
+      xrow[tid] = r < n ? h + (gathered ? p.row_idx[r] : r) * p.ld_h : nullptr;
+      ss_s[tid] = 0.f;
+      t_s[tid] = 0.f;
+    }
+    __syncthreads();
+    for (int j0 = 0; j0 < p.b; j0 += kSJ) {
+      float acc[kWRT][4];
+#pragma unroll
+      for (int i = 0; i < kWRT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+      gemm_wide<XT>(xrow, W, p.d, j0, p.b, p.d, acc, sm_f, sm_f + kWR * kVP, ss_s);
+#pragma unroll
+      for (int i = 0; i < kWRT; ++i) {
+        const int r = ty + 8 * i;
+        const float scale = rms_scale(ss_s[r], p.inv_d, p.eps);
+        float part = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int j = j0 + tx + 32 * c;
+          if (j < p.b) part = fmaf(p.w_up[j], silu_f32(__fmul_rn(acc[i][c], scale)), part);
+        }
+        part = warp_sum_f32(part);
+        if (tx == 0) t_s[r] += part;
+      }
+      __syncthreads();
+    }
+    if (ty == 0) {
+      // two 32-row words: decisions, then one look-back for the block
+      uint32_t bits[2];
+      bool exr[2];
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const int64_t r = r0 + 32 * w + tx;
+        bool ex = false;
+        if (r < n) {
+          const float t = t_s[32 * w + tx];
+          const float score = score_from_logit(t);
+          ex = score > p.theta;
+          if (p.scores) p.scores[r] = score;
+          if (p.logits) p.logits[r] = t;
+          if (p.mask) p.mask[r] = ex ? 1 : 0;
+          if (ex && p.exit_layers) p.exit_layers[gathered ? p.row_idx[r] : r] = p.layer;
+        }
+        exr[w] = ex;
+        bits[w] = __ballot_sync(0xffffffffu, ex);
+      }
+      if (p.exit_idx || p.cont_idx || p.counts) {
+        const uint32_t agg = __popc(bits[0]) + __popc(bits[1]);
+        const uint32_t E = lookback_exclusive(p.ws->status, tag, blk, agg);
+        const uint32_t lt = (1u << tx) - 1u;
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          const int64_t r = r0 + 32 * w + tx;
+          if (r < n) {
+            const int64_t rank = (int64_t)E + (w ? __popc(bits[0]) : 0) + __popc(bits[w] & lt);
+            const int64_t id = (p.ids_from_rows && gathered) ? p.row_idx[r] : r;
+            if (exr[w]) {
+              if (p.exit_idx) p.exit_idx[rank] = id;
+            } else if (p.cont_idx) {
+              p.cont_idx[r - rank] = id;
+            }
+          }
+        }
+        if (blk == nblk - 1 && tx == 0 && p.counts) {
+          p.counts[0] = (int64_t)E + agg;
+          p.counts[1] = n - ((int64_t)E + agg);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (nblk == 0 && blockIdx.x == 0 && tid == 0 && p.counts) {
+    p.counts[0] = 0;
+    p.counts[1] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) launch_done(p.ws);
+}
+
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
   if (a.b < 1 || a.d < 1) return set_error(TIDE_ERR_ARG, "empty router");
   SimtParams p{};
@@ -337,6 +532,33 @@ int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
     attr = true;
   }
   void (*kern)(const SimtParams) = nullptr;
+  // many rows: the 64-row FMA-bound kernel once it still fills every SM
+  static bool wide_attr = false;
+  if (!wide_attr) {
+    cudaFuncSetAttribute(route_simt_wide_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+    cudaFuncSetAttribute(route_simt_wide_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+    cudaFuncSetAttribute(route_simt_wide_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+    wide_attr = true;
+  }
+  const char* wenv = getenv("TIDE_SIMT_WIDE_ROWS");
+  // measured (tools/tf32_probe.py, f32): 8,192 x 768 100 -> 64 us, 65,536 x
+  // 4096 3.26 -> 1.87 ms; at 2,048 rows (32 CTAs) the 16-row kernel wins
+  const int64_t wide_rows = wenv ? atoll(wenv) : (int64_t)sm_count(dev) * 48;
+  if (vec && a.n >= wide_rows) {
+    switch (a.dtype) {
+      case TIDE_F32: kern = route_simt_wide_kernel<float>; break;
+      case TIDE_BF16: kern = route_simt_wide_kernel<__nv_bfloat16>; break;
+      default: kern = route_simt_wide_kernel<__half>; break;
+    }
+    const int64_t wblk = (a.n + kWR - 1) / kWR;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSThreads, kWSmem) !=
+            cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>(wblk, (int64_t)sm_count(dev) * per_sm));
+    kern<<<wgrid, kSThreads, kWSmem, stream>>>(p);
+    return check_launch("route_simt_wide_kernel");
+  }
   switch (a.dtype) {
     case TIDE_F32: kern = vec ? route_simt_kernel<float, true> : route_simt_kernel<float, false>; break;
     case TIDE_BF16:

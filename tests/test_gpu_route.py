@@ -341,3 +341,23 @@ def test_f32_tensor_core_opt_in(n, d, b, monkeypatch):
     e, c = O.compact_indices(r["mask"].cpu().numpy())
     np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
     np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("dtype,n,d,b", [("f32", 9000, 768, 128), ("f32", 7200, 100, 40),
+                                         ("bf16", 8000, 512, 300)])
+def test_wide_cuda_core_kernel(dtype, n, d, b):
+    """64-row CUDA-core kernel (n above its threshold): f32 rows, a ragged
+    width / bottleneck, and a bf16 shape the tensor-core kernel does not take
+    (b > 256); compaction bit-exact."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(n + d + b))
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = O.round_to(g.standard_normal((n, d), dtype=np.float32), dtype)
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, dtype), _router(wd, wu), theta=0.5, want_logits=True,
+                want_indices=True)
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, dtype, f"wide n={n}")
+    e, c = O.compact_indices(r["mask"].cpu().numpy())
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)

@@ -201,6 +201,48 @@ def _decode_plan(bank, ckpts, code, dev):
     return arrays
 
 
+class _ChainGraphs:
+    """Replay cache of per-token peeling chains.
+
+    The chain is several launches per call (one per checkpoint, the tail,
+    its resolve) whose host issue cost (~130 us at config 2) exceeds their
+    device time (~93 us).  The second eager call with the same capture
+    buffers (device pointers, shapes, dtype), bank routers and config records
+    the chain into a CUDA graph; later calls replay it and return a copy of
+    its output.  The key holds the data pointers only, so a replay reads
+    whatever the caller's tensors at those addresses hold now — the same
+    contract as a captured model step."""
+
+    def __init__(self, size: int = 8):
+        from collections import OrderedDict
+        self.size = size
+        self.entries = OrderedDict()   # key -> [calls, graph, output, keepalive]
+        self.streams = {}
+
+    @staticmethod
+    def enabled() -> bool:
+        import os
+        return os.environ.get("TIDE_CHAIN_GRAPHS", "1") != "0"
+
+    @staticmethod
+    def knobs() -> tuple:
+        """Environment switches that change the recorded launch sequence."""
+        import os
+        e = os.environ
+        return tuple(e.get(k) for k in ("TIDE_CHAIN_TAIL", "TIDE_TAIL_AFTER", "TIDE_TAIL_ROWS",
+                                        "TIDE_TAIL_KS", "TIDE_SPLIT", "TIDE_PDL"))
+
+    def stream(self, dev):
+        st = self.streams.get(dev.index)
+        if st is None:
+            st = self.streams[dev.index] = torch.cuda.Stream(dev)
+            D.workspace(dev, st.cuda_stream)  # allocated outside any capture
+        return st
+
+
+_chain_graphs = _ChainGraphs()
+
+
 def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
                  staged=None, dev=None):
     """Exit map only (int64 CUDA tensor [n]); the hot path of posthoc_select."""
@@ -208,6 +250,41 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
     ckpts = [k for k in bank.checkpoints if k >= config.k_min]
     if staged is None:
         staged, dev = _stage_layers(hidden_states, [k + 1 for k in ckpts] + [L])
+    final = staged[L]
+    n = final.shape[0]
+    if (config.mode == PER_TOKEN and n > N.MAX_DECODE_ROWS and len(ckpts) > 1
+            and _ChainGraphs.enabled() and not torch.cuda.is_current_stream_capturing()):
+        routers = [bank.routers[k] for k in ckpts]
+        key = (id(bank), tuple(ckpts), float(config.exit_threshold), float(bank.eps),
+               final.dtype, tuple(final.shape), D.stream_handle(dev),
+               tuple(staged[k + 1].data_ptr() for k in ckpts) + (final.data_ptr(),),
+               tuple((id(r), id(r.w_down), id(r.w_up)) for r in routers),
+               _ChainGraphs.knobs())
+        cache = _chain_graphs.entries
+        ent = cache.get(key)
+        if ent is not None and ent[1] is not None:
+            cache.move_to_end(key)
+            ent[1].replay()
+            return ent[2].clone()
+        if ent is None:
+            cache[key] = [1, None, None, (bank, routers)]
+            while len(cache) > _chain_graphs.size:
+                cache.popitem(last=False)
+        else:
+            # second call with these buffers: record the chain, then replay it
+            g = torch.cuda.CUDAGraph()
+            st = _chain_graphs.stream(dev)
+            st.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.graph(g, stream=st):
+                out = _select_exits_chain(staged, bank, config, ckpts, dev)
+            ent[1], ent[2] = g, out
+            g.replay()
+            return out.clone()
+    return _select_exits_chain(staged, bank, config, ckpts, dev)
+
+
+def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev):
+    L = bank.num_layers
     final = staged[L]
     n, d = final.shape
     if not ckpts or n == 0:

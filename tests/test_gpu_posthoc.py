@@ -310,3 +310,31 @@ def test_chain_captured_in_cuda_graph(d, n, L, scale, theta):
         torch.cuda.synchronize()
         want = P.select_exits(states, bank, cfg)
         assert torch.equal(out, want), rep
+
+
+@pytest.mark.parametrize("d,n,L,scale,theta", [(4096, 4096, 32, 0.1, 0.5), (8192, 2048, 40, 0.06, 0.7)])
+def test_eager_chain_graph_cache(d, n, L, scale, theta, monkeypatch):
+    """Repeated eager select_exits calls with the same capture buffers replay a
+    recorded chain: same exit map as the uncached path, new contents of the
+    buffers are read, a returned map is not overwritten by the next call."""
+    need_gpu()
+    from paper_2603_21365_b200 import runtime as R
+    ckpts, routers, states, bank, head = _big_case(L, d, n, "bf16", 300 + n, scale=scale)
+    cfg = P.RuntimeConfig(exit_threshold=theta)
+    R._chain_graphs.entries.clear()
+    first = P.select_exits(states, bank, cfg)     # eager, counted
+    second = P.select_exits(states, bank, cfg)    # recorded + replayed
+    third = P.select_exits(states, bank, cfg)     # replayed
+    assert len(R._chain_graphs.entries) == 1
+    assert next(iter(R._chain_graphs.entries.values()))[1] is not None
+    assert torch.equal(first, second) and torch.equal(first, third)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(77)
+    for k in ckpts:
+        states[k + 1].copy_(torch.randn(states[k + 1].shape, generator=gen,
+                                        device="cuda").to(states[k + 1].dtype))
+    replayed = P.select_exits(states, bank, cfg)
+    monkeypatch.setenv("TIDE_CHAIN_GRAPHS", "0")
+    eager = P.select_exits(states, bank, cfg)
+    assert torch.equal(replayed, eager)
+    assert torch.equal(third, first)  # earlier results are copies

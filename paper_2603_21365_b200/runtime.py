@@ -252,6 +252,29 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
         staged, dev = _stage_layers(hidden_states, [k + 1 for k in ckpts] + [L])
     final = staged[L]
     n = final.shape[0]
+    if 0 < n <= N.MAX_DECODE_ROWS and ckpts:
+        # decode step: the bound launch of these buffers / routers / config,
+        # built once (the argument block of tide_route_decode minus the
+        # output pointer), then one ctypes call per step
+        s = D.stream_handle(dev)
+        routers = [bank.routers[k] for k in ckpts]
+        key = (id(bank), tuple(ckpts), float(config.exit_threshold), config.mode,
+               config.k_min, final.dtype, tuple(final.shape), s,
+               tuple(staged[k + 1].data_ptr() for k in ckpts),
+               tuple((id(r), id(r.w_down), id(r.w_up)) for r in routers))
+        hit = _decode_calls.get(key)
+        if hit is None:
+            hit = _bind_decode(staged, bank, config, ckpts, dev, s, routers)
+            if len(_decode_calls) >= 64:
+                _decode_calls.clear()
+            _decode_calls[key] = hit
+        if hit[0] is not None:
+            out = torch.empty((n,), dtype=torch.int64, device=dev)
+            args = hit[0]
+            rc = hit[1](*args[:16], out.data_ptr(), *args[17:])
+            if rc:
+                N.check(rc, "tide_route_decode")
+            return out
     if (config.mode == PER_TOKEN and n > N.MAX_DECODE_ROWS and len(ckpts) > 1
             and _ChainGraphs.enabled() and not torch.cuda.is_current_stream_capturing()):
         routers = [bank.routers[k] for k in ckpts]
@@ -281,6 +304,29 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
             g.replay()
             return out.clone()
     return _select_exits_chain(staged, bank, config, ckpts, dev)
+
+
+_decode_calls: dict = {}
+
+
+def _bind_decode(staged, bank, config, ckpts, dev, s, routers):
+    """(argument tuple, C function) of the decode launch, or (None, None) when
+    the shape takes the chain path (misaligned rows / width)."""
+    final = staged[bank.num_layers]
+    n, d = final.shape
+    code = D.dtype_code(final)
+    vec = 4 if code == N.F32 else 8
+    if d % vec or any(staged[k + 1].data_ptr() % 16 for k in ckpts):
+        return (None, None, routers)
+    w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)
+    b = bank.bottleneck if hasattr(bank, "bottleneck") else routers[0].bottleneck
+    mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
+    args = (N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
+            w_arr, u_arr, b, l_arr, float(np.float32(bank.eps)),
+            float(np.float32(config.exit_threshold)), int(config.k_min), mode, None, None,
+            0, None, D.workspace(dev, s).data_ptr(), s)
+    # keep the routers alive with the entry so their ids stay unique
+    return (args, N.load().tide_route_decode, routers)
 
 
 def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev):

@@ -200,7 +200,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(x["seconds"] for x in runs) / len(runs),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": workload_config(1), "impl": "reference",
+            "data": "synthetic", "config": workload_config(max(1, args.gpus)), "impl": "reference",
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": runs[-1]["cores"],
                              "kind": "port", "sample": runs[-1]["sample"]},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -219,10 +219,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TIDE_BENCH_ONE_GPU=1 (flow test of the N > 1 path on a one-GPU box):
+    # every rank on cuda:0, gloo instead of NCCL — timings meaningless
+    one_gpu = os.environ.get("TIDE_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_2603_21365_b200 as P
     from paper_2603_21365_b200 import _device as Dv
@@ -253,7 +261,7 @@ def run_ours(args):
     ws = Dv.workspace(dev).data_ptr()
     launches = {"n": 0}
 
-    def step(kernel_events=None):
+    def step(kernel_events=None, collective=True):
         if kernel_events is not None:
             kernel_events[0].record(stream)
         rc = lib.tide_route(h.data_ptr(), D, N_TOK, None, N_TOK, D, N.BF16, None, wd.data_ptr(),
@@ -265,7 +273,7 @@ def run_ours(args):
             kernel_events[1].record(stream)
         if rc:
             N.check(rc, "tide_route")
-        if gathered is not None:
+        if gathered is not None and collective:
             gathered.all_gather()  # C1 + C2 in one collective
 
     def barrier():
@@ -299,9 +307,12 @@ def run_ours(args):
     sustained.start()
     t_end = time.time() + 0.6
     while time.time() < t_end:
+        # kernel only: ranks leave this wall-clock loop after different
+        # iteration counts, so no collective may be issued in it
         for _ in range(50):
-            step()
+            step(collective=False)
         torch.cuda.synchronize(dev)
+    barrier()
     clk_sustained = sustained.stop()
     # parity spot-check of the final state on rank 0 (first 2,048 rows vs the oracle)
     if rank == 0 and not args.no_check:
@@ -340,6 +351,8 @@ def run_ours(args):
                             None, mask.data_ptr(), exit_idx.data_ptr(), cont_idx.data_ptr(), 0,
                             None, counts.data_ptr(), ws, sh)
         N.check(rc, "tide_route")
+        if gathered is not None:
+            gathered.all_gather()  # the same step as the device-resident one
         mask_host.copy_(mask, non_blocking=True)
         idx_host.copy_(exit_idx, non_blocking=True)
         cnt_host.copy_(counts, non_blocking=True)
@@ -390,7 +403,7 @@ def run_ours(args):
                       "tflops_tensor": 2.0 * D * B * N_TOK / (kavg / 1e3) / 1e12,
                       "kernel_ms_min": min(kernel_ms), "kernel_ms_max": max(kernel_ms)},
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the host baseline: rank 0 at N = 1
             line["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(
                 float(os.environ.get("TIDE_CPU_BASELINE_S", "10"))).items()
                 if k in ("value", "unit", "cores", "kind", "sample")}

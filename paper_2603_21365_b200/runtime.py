@@ -285,7 +285,7 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
                _ChainGraphs.knobs())
         cache = _chain_graphs.entries
         ent = cache.get(key)
-        if ent is not None and ent[1] is not None:
+        if ent is not None and ent[1]:
             cache.move_to_end(key)
             ent[1].replay()
             return ent[2].clone()
@@ -293,13 +293,18 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
             cache[key] = [1, None, None, (bank, routers)]
             while len(cache) > _chain_graphs.size:
                 cache.popitem(last=False)
-        else:
+        elif ent[1] is None:
             # second call with these buffers: record the chain, then replay it
             g = torch.cuda.CUDAGraph()
             st = _chain_graphs.stream(dev)
             st.wait_stream(torch.cuda.current_stream(dev))
-            with torch.cuda.graph(g, stream=st):
-                out = _select_exits_chain(staged, bank, config, ckpts, dev)
+            try:
+                with torch.cuda.graph(g, stream=st):
+                    out = _select_exits_chain(staged, bank, config, ckpts, dev)
+            except Exception:  # not capturable here: stay eager for this key
+                ent[1] = False
+                torch.cuda.synchronize(dev)
+                return _select_exits_chain(staged, bank, config, ckpts, dev)
             ent[1], ent[2] = g, out
             g.replay()
             return out.clone()

@@ -193,7 +193,8 @@ int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_
  * links must read (0 when the tail handled the rows, else *n_dev), so links
  * launched after it with n_dev = tail_count become no-ops (or are skipped
  * entirely inside a captured CUDA graph, see tide_capture_cond_*).  scores: device
- * scratch of C * cap f32 (cap = the chain's row capacity).  bf16 / f16.
+ * scratch of C * cap f32 (cap = the chain's row capacity).  bf16 / f16
+ * (split-K tensor-core kernel) or f32 (CUDA-core kernel, f32 products).
  * (No reference counterpart: an execution strategy of posthoc_select.)
  */
 int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t rows_total,

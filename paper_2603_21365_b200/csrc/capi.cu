@@ -144,9 +144,10 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
     return set_error(TIDE_ERR_ARG, "tide_route_tail: bad shape");
   if (!row_idx || !n_dev || !scores || !exit_layers || !tail_count || !workspace)
     return set_error(TIDE_ERR_ARG, "tide_route_tail: null device buffer");
-  if (dtype != TIDE_F16 && dtype != TIDE_BF16)
-    return set_error(TIDE_ERR_UNSUPPORTED, "tide_route_tail: bf16 / f16 captures only");
-  if (!route_tc_supported(dtype, d, b)) return set_error(TIDE_ERR_UNSUPPORTED, "tide_route_tail: shape");
+  if (dtype != TIDE_F32 && dtype != TIDE_F16 && dtype != TIDE_BF16)
+    return set_error(TIDE_ERR_ARG, "tide_route_tail: bad dtype %d", dtype);
+  if (dtype != TIDE_F32 && !route_tc_supported(dtype, d, b))
+    return set_error(TIDE_ERR_UNSUPPORTED, "tide_route_tail: shape");
   for (int c = 0; c < C; ++c)
     if (((reinterpret_cast<uintptr_t>(h_ptrs[c]) | reinterpret_cast<uintptr_t>(w_ptrs[c])) & 15) ||
         (c && layers[c] <= layers[c - 1]))
@@ -168,6 +169,10 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
   a.scores = scores;
   a.exit_layers = exit_layers;
   a.workspace = workspace;
+  if (dtype == TIDE_F32)  // CUDA-core kernel, f32 products (the 1e-5 contract)
+    return route_simt_tail_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, layers, n_limit, tail_count,
+                                  (unsigned long long)cond_handle,
+                                  reinterpret_cast<cudaStream_t>(stream));
   return route_tcs_tail_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, layers, n_limit, tail_count,
                                (unsigned long long)cond_handle, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -52,6 +52,14 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                           const int64_t* layers, int64_t n_limit, int64_t* tail_count,
                           unsigned long long cond, cudaStream_t stream);
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream);
+int route_simt_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
+                           const void* const* w_ptrs, const float* const* wup_ptrs,
+                           const int64_t* layers, int64_t n_limit, int64_t* tail_count,
+                           unsigned long long cond, cudaStream_t stream);
+int chain_resolve_launch(const float* scores, int64_t cap, int C, const int64_t* layers,
+                         float theta, const int64_t* n_dev, int64_t n_limit,
+                         const int64_t* row_idx, int64_t* exit_layers, int64_t* tail_count,
+                         unsigned long long cond, cudaStream_t stream);
 bool route_tf32_supported(int d, int b);
 int route_tf32_launch(const RouteArgs& a, cudaStream_t stream);
 int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,

@@ -490,6 +490,164 @@ __global__ void __launch_bounds__(kSThreads, 1) route_simt_wide_kernel(const Sim
   if (tid == 0) launch_done(p.ws);
 }
 
+// Chain tail for f32 rows (tide_route_tail): the live rows (row_idx[0 ..
+// *n_dev)) scored against C checkpoints in ONE launch (grid.y = checkpoint),
+// scores [C, cap]; the resolve kernel (route_tcs.cu) then picks each row's
+// first firing checkpoint.  Nothing is routed when *n_dev > n_limit.
+constexpr int kSimtTailC = 32;
+struct SimtTailParams {
+  SimtParams base;
+  const void* hs[kSimtTailC];
+  const void* ws[kSimtTailC];
+  const float* wups[kSimtTailC];
+  int64_t cap, n_limit;
+};
+
+template <typename XT>
+__global__ void __launch_bounds__(kSThreads) route_simt_tail_kernel(const __grid_constant__ SimtTailParams tp) {
+  const SimtParams& p = tp.base;
+  extern __shared__ float sm_f[];
+  __shared__ float ss_s[kSR];
+  __shared__ float t_s[kSR];
+  __shared__ const XT* xrow[kSR];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int c = blockIdx.y;
+  const int64_t n = *p.n_dev;
+  if (n > tp.n_limit) return;
+  const XT* h = reinterpret_cast<const XT*>(tp.hs[c]);
+  const XT* W = reinterpret_cast<const XT*>(tp.ws[c]);
+  const float* w_up = tp.wups[c];
+  const int64_t nblk = (n + kSR - 1) / kSR;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t r0 = blk * kSR;
+    if (tid < kSR) {
+      const int64_t r = r0 + tid;
+      xrow[tid] = r < n ? h + p.row_idx[r] * p.ld_h : nullptr;
+      ss_s[tid] = 0.f;
+      t_s[tid] = 0.f;
+    }
+    __syncthreads();
+    for (int j0 = 0; j0 < p.b; j0 += kSJ) {
+      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      gemm_16x128_vec<XT>(xrow, W, p.d, j0, p.b, p.d, acc, sm_f, sm_f + kSR * kVP, ss_s);
+#pragma unroll
+      for (int r2 = 0; r2 < 2; ++r2) {
+        const int r = ty + 8 * r2;
+        const float scale = rms_scale(ss_s[r], p.inv_d, p.eps);
+        float part = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int j = j0 + tx + 32 * cc;
+          if (j < p.b) part = fmaf(w_up[j], silu_f32(__fmul_rn(acc[r2][cc], scale)), part);
+        }
+        part = warp_sum_f32(part);
+        if (tx == 0) t_s[r] += part;
+      }
+      __syncthreads();
+    }
+    if (ty == 0 && tx < kSR && r0 + tx < n)
+      p.scores[(size_t)c * tp.cap + r0 + tx] = score_from_logit(t_s[tx]);
+    __syncthreads();
+  }
+}
+
+// Same, 64 rows per CTA (gemm_wide): fewer, FMA-bound CTAs.
+template <typename XT>
+__global__ void __launch_bounds__(kSThreads, 1) route_simt_tail_wide_kernel(const __grid_constant__ SimtTailParams tp) {
+  const SimtParams& p = tp.base;
+  extern __shared__ float sm_f[];
+  __shared__ float ss_s[kWR];
+  __shared__ float t_s[kWR];
+  __shared__ const XT* xrow[kWR];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int c = blockIdx.y;
+  const int64_t n = *p.n_dev;
+  if (n > tp.n_limit) return;
+  const XT* h = reinterpret_cast<const XT*>(tp.hs[c]);
+  const XT* W = reinterpret_cast<const XT*>(tp.ws[c]);
+  const float* w_up = tp.wups[c];
+  const int64_t nblk = (n + kWR - 1) / kWR;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t r0 = blk * kWR;
+    if (tid < kWR) {
+      const int64_t r = r0 + tid;
+      xrow[tid] = r < n ? h + p.row_idx[r] * p.ld_h : nullptr;
+      ss_s[tid] = 0.f;
+      t_s[tid] = 0.f;
+    }
+    __syncthreads();
+    for (int j0 = 0; j0 < p.b; j0 += kSJ) {
+      float acc[kWRT][4];
+#pragma unroll
+      for (int i = 0; i < kWRT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+      gemm_wide<XT>(xrow, W, p.d, j0, p.b, p.d, acc, sm_f, sm_f + kWR * kVP, ss_s);
+#pragma unroll
+      for (int i = 0; i < kWRT; ++i) {
+        const int r = ty + 8 * i;
+        const float scale = rms_scale(ss_s[r], p.inv_d, p.eps);
+        float part = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int j = j0 + tx + 32 * cc;
+          if (j < p.b) part = fmaf(w_up[j], silu_f32(__fmul_rn(acc[i][cc], scale)), part);
+        }
+        part = warp_sum_f32(part);
+        if (tx == 0) t_s[r] += part;
+      }
+      __syncthreads();
+    }
+    if (tid < kWR && r0 + tid < n) p.scores[(size_t)c * tp.cap + r0 + tid] = score_from_logit(t_s[tid]);
+    __syncthreads();
+  }
+}
+
+int route_simt_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
+                           const void* const* w_ptrs, const float* const* wup_ptrs,
+                           const int64_t* layers, int64_t n_limit, int64_t* tail_count,
+                           unsigned long long cond, cudaStream_t stream) {
+  if (C < 1 || C > kSimtTailC) return set_error(TIDE_ERR_ARG, "tail: C must be in [1, %d]", kSimtTailC);
+  if (a.d % 4 || a.ld_h % 4) return set_error(TIDE_ERR_UNSUPPORTED, "f32 tail: d and ld_h must be multiples of 4");
+  SimtTailParams tp{};
+  SimtParams& p = tp.base;
+  p.n_dev = a.n_dev;
+  p.d = a.d;
+  p.b = a.b;
+  p.ld_h = a.ld_h;
+  p.row_idx = a.row_idx;
+  p.eps = a.eps;
+  p.inv_d = (float)(1.0 / (double)a.d);
+  p.theta = a.theta;
+  p.scores = a.scores;
+  for (int c = 0; c < C; ++c) {
+    tp.hs[c] = h_ptrs[c];
+    tp.ws[c] = w_ptrs[c];
+    tp.wups[c] = wup_ptrs[c];
+  }
+  tp.cap = a.n;
+  tp.n_limit = std::min<int64_t>(n_limit, a.n);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(route_simt_tail_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVSmem);
+    cudaFuncSetAttribute(route_simt_tail_wide_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+    attr = true;
+  }
+  const char* wenv = getenv("TIDE_F32_TAIL_WIDE");
+  const bool wide = wenv ? wenv[0] == '1' : true;
+  int rc;
+  if (wide) {
+    const int64_t nblk = std::max<int64_t>(1, (tp.n_limit + kWR - 1) / kWR);
+    route_simt_tail_wide_kernel<float><<<dim3((unsigned)nblk, (unsigned)C), kSThreads, kWSmem, stream>>>(tp);
+    rc = check_launch("route_simt_tail_wide_kernel");
+  } else {
+    const int64_t nblk = std::max<int64_t>(1, (tp.n_limit + kSR - 1) / kSR);
+    route_simt_tail_kernel<float><<<dim3((unsigned)nblk, (unsigned)C), kSThreads, kVSmem, stream>>>(tp);
+    rc = check_launch("route_simt_tail_kernel");
+  }
+  if (rc) return rc;
+  return chain_resolve_launch((const float*)a.scores, a.n, C, layers, a.theta, a.n_dev,
+                              tp.n_limit, a.row_idx, a.exit_layers, tail_count, cond, stream);
+}
+
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {
   if (a.b < 1 || a.d < 1) return set_error(TIDE_ERR_ARG, "empty router");
   SimtParams p{};

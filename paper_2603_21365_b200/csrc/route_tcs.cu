@@ -833,13 +833,21 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
   }
   if ((rc = tcs_launch<kMaxTailC>(a, p, wm, L.smem_bytes, ks, grid, C, stream, "route_tcs_kernel (tail)")))
     return rc;
+  return chain_resolve_launch((const float*)a.scores, a.n, C, layers, a.theta, a.n_dev, n_limit,
+                              a.row_idx, a.exit_layers, tail_count, cond, stream);
+}
+
+int chain_resolve_launch(const float* scores, int64_t cap, int C, const int64_t* layers,
+                         float theta, const int64_t* n_dev, int64_t n_limit,
+                         const int64_t* row_idx, int64_t* exit_layers, int64_t* tail_count,
+                         unsigned long long cond, cudaStream_t stream) {
+  if (C < 1 || C > kMaxTailC) return set_error(TIDE_ERR_ARG, "resolve: C must be in [1, %d]", kMaxTailC);
   TailLayers tl{};
   for (int c = 0; c < C; ++c) tl.l[c] = layers[c];
   // plain launch (full dependency): a conditional graph node may follow it
   const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_limit + 255) / 256, 148));
-  chain_resolve_kernel<<<nb, 256, 0, stream>>>((const float*)a.scores, (int64_t)a.n, C, tl, a.theta,
-                                               a.n_dev, n_limit, a.row_idx, a.exit_layers,
-                                               tail_count, cond);
+  chain_resolve_kernel<<<nb, 256, 0, stream>>>(scores, cap, C, tl, theta, n_dev, n_limit, row_idx,
+                                               exit_layers, tail_count, cond);
   return check_launch("chain_resolve_kernel");
 }
 

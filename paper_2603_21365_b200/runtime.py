@@ -230,7 +230,8 @@ class _ChainGraphs:
         import os
         e = os.environ
         return tuple(e.get(k) for k in ("TIDE_CHAIN_TAIL", "TIDE_TAIL_AFTER", "TIDE_TAIL_ROWS",
-                                        "TIDE_TAIL_KS", "TIDE_SPLIT", "TIDE_PDL"))
+                                        "TIDE_TAIL_KS", "TIDE_SPLIT", "TIDE_PDL",
+                                        "TIDE_F32_TAIL_ROWS"))
 
     def stream(self, dev):
         st = self.streams.get(dev.index)
@@ -371,6 +372,23 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev):
                 exit_layers.fill_(k)
                 break
         return exit_layers
+    if code == N.F32 and len(ckpts) >= 2 and n <= _f32_tail_rows() and _tail_enabled():
+        # f32 rows, few of them: each CUDA-core link costs its full latency
+        # whatever its row count, so score every checkpoint for every row in
+        # ONE launch and resolve the first firing one (same map as peeling:
+        # a row's score at checkpoint k depends only on that row)
+        wts = [device_weights(bank.routers[k], code, dev) for k in ckpts]
+        every = torch.arange(n, dtype=torch.int64, device=dev)
+        n_t = torch.full((1,), n, dtype=torch.int64, device=dev)
+        scratch = torch.empty(len(ckpts) * n, dtype=torch.float32, device=dev)
+        tail_count = torch.empty(1, dtype=torch.int64, device=dev)
+        N.check(lib.tide_route_tail(
+            N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
+            every.data_ptr(), n_t.data_ptr(), n, n, N.ptr_array([w.data_ptr() for w, _ in wts]),
+            N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(ckpts), eps, theta,
+            scratch.data_ptr(), exit_layers.data_ptr(), tail_count.data_ptr(), 0, ws, s),
+            "tide_route_tail")
+        return exit_layers
     rem = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
     cnt = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(2)]
     row_idx, n_dev = 0, 0
@@ -408,6 +426,11 @@ TAIL_AFTER = 3  # links of the peeling chain before the tail attempt
 def _tail_enabled() -> bool:
     import os
     return os.environ.get("TIDE_CHAIN_TAIL", "1") != "0"
+
+
+def _f32_tail_rows() -> int:
+    import os
+    return int(os.environ.get("TIDE_F32_TAIL_ROWS", 4096))
 
 
 def _tail_after() -> int:

@@ -67,9 +67,9 @@ def test_argument_errors_are_reported_not_computed(lib):
     rc = lib.tide_route_tail(one, 1, 64, 10, 64, N.BF16, None, 16, 10, 10, one, one, 128,
                              N.i64_array([3]), 1e-6, 0.5, 16, 16, 16, 0, 16, None)
     assert rc == -1 and "null device buffer" in lib.tide_last_error().decode()
-    rc = lib.tide_route_tail(one, 1, 64, 10, 64, N.F32, 16, 16, 10, 10, one, one, 128,
+    rc = lib.tide_route_tail(one, 1, 64, 10, 64, 7, 16, 16, 10, 10, one, one, 128,
                              N.i64_array([3]), 1e-6, 0.5, 16, 16, 16, 0, 16, None)
-    assert rc == -2 and "bf16 / f16" in lib.tide_last_error().decode()
+    assert rc == -1 and "bad dtype" in lib.tide_last_error().decode()
     two = N.ptr_array([16, 32])
     rc = lib.tide_route_tail(two, 2, 64, 10, 64, N.BF16, 16, 16, 10, 10, two, two, 128,
                              N.i64_array([7, 3]), 1e-6, 0.5, 16, 16, 16, 0, 16, None)

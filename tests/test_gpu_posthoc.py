@@ -338,3 +338,33 @@ def test_eager_chain_graph_cache(d, n, L, scale, theta, monkeypatch):
     eager = P.select_exits(states, bank, cfg)
     assert torch.equal(replayed, eager)
     assert torch.equal(third, first)  # earlier results are copies
+
+
+@pytest.mark.parametrize("n,d,L,theta", [(2048, 768, 12, 0.5), (3000, 512, 24, 0.55),
+                                         (500, 772, 16, 1.0)])
+def test_f32_chain_all_checkpoints_at_once(n, d, L, theta, monkeypatch):
+    """f32 rows, few of them: one CUDA-core launch scores every checkpoint and
+    the resolve kernel picks the first firing one — the same exit map as the
+    peeling links (and the oracle, to the f32 band)."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(n + d + L))
+    ckpts = O.checkpoint_layers(L, 4)
+    routers = {k: O.make_router(d, 128, k, g, scale=0.2) for k in ckpts}
+    states = [torch.from_numpy(g.standard_normal((n, d), dtype=np.float32)).cuda()
+              for _ in range(L + 1)]
+    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L)
+    cfg = P.RuntimeConfig(exit_threshold=theta)
+    scores, exc = {}, np.zeros(n, bool)
+    for k in ckpts:
+        s_, t, m = O.route_logits(states[k + 1].cpu().numpy(), routers[k])
+        scores[k] = s_
+        exc |= np.abs(t - O.logit_of(theta)) <= RTOL["f32"] * np.maximum(np.abs(t), m)
+    want = O.first_exit_from_scores(scores, theta)
+    monkeypatch.setenv("TIDE_CHAIN_GRAPHS", "0")
+    got = P.select_exits(states, bank, cfg).cpu().numpy()
+    monkeypatch.setenv("TIDE_CHAIN_TAIL", "0")
+    links = P.select_exits(states, bank, cfg).cpu().numpy()
+    assert np.all((got == want) | exc) and np.all((links == want) | exc)
+    assert np.array_equal(got, links)
+    if theta == 1.0:
+        assert np.all(got == P.NO_EXIT)

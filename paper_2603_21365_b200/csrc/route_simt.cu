@@ -374,7 +374,7 @@ __device__ __forceinline__ void gemm_wide(const XT* const* xrow, const XT* W, in
         if (part == 0) ss_s[r] += sq;
       }
     }
-#pragma unroll 2
+#pragma unroll
     for (int kk = 0; kk < kVK; kk += 4) {
       float4 w[4];
 #pragma unroll

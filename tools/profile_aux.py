@@ -29,10 +29,11 @@ torch.cuda.synchronize()
 # router training (§8f-4): one epoch at d = 4096 (per-row activation / Adam kernels)
 x = torch.randn((4096, 4096), device="cuda")
 P.train_router(x, (x[:, 0] > 0).float(), 3, P.CalibrationConfig(epochs=1, batch_size=1024))
-# opt-in 3xTF32 f32 router kernel at 16,384 x 4096
-os.environ["TIDE_F32_TC"] = "1"
+# f32 router at 16,384 x 4096: the 64-row CUDA-core kernel, then the opt-in 3xTF32 one
 h = torch.randn((16384, 4096), device="cuda")
 r = O.make_router(4096, 128, 3, g)
+P.route(h, P.Router(layer=3, w_down=r.w_down, w_up=r.w_up), theta=0.5, want_indices=True)
+os.environ["TIDE_F32_TC"] = "1"
 P.route(h, P.Router(layer=3, w_down=r.w_down, w_up=r.w_up), theta=0.5, want_indices=True)
 os.environ.pop("TIDE_F32_TC")
 torch.cuda.synchronize()

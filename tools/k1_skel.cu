@@ -373,13 +373,14 @@ int main(int argc, char** argv) {
     printf("%-58s %8.1f us  %6.0f GB/s\n", name, us, bytes / us / 1e3);
   };
   struct Cfg { int na, nw; };
-  for (Cfg c : {Cfg{9, 4}, Cfg{8, 4}}) {
+  for (Cfg c : {Cfg{9, 4}}) {
     p.na = c.na;
     p.nw = c.nw;
     char nm[128];
-    for (uint32_t f : {4u, 132u, 7u, 135u}) {
+    // flag 8: W loaded once (first nw chunks), no per-chunk W re-reads from L2
+    for (uint32_t f : {4u, 12u, 7u, 15u, 7u, 15u}) {
       p.flags = f;
-      const char* fs = f == 4 ? "TMA" : f == 132 ? "TMA quad-order" : f == 7 ? "TMA+MMA+RMS" : "TMA+MMA+RMS quad";
+      const char* fs = f == 4 ? "TMA" : f == 12 ? "TMA, no W reload" : f == 7 ? "TMA+MMA+RMS" : "TMA+MMA+RMS no W rel";
       snprintf(nm, sizeof nm, "na=%d nw=%d %-16s CM0 NR8 RL0 (base)", c.na, c.nw, fs);
       show(nm, run<0, 8, 0>(th, tw, p, sms));
 

@@ -83,16 +83,47 @@ def assemble_partition(local_lists, local_counts, offsets):
     return torch.cat(ex), torch.cat(co)
 
 
-def gather_exit_layers(local_exit_layers: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """C1 for unequal shards: pad to the largest shard, all-gather, strip."""
-    n_local = torch.tensor([local_exit_layers.numel()], dtype=torch.int64,
-                           device=local_exit_layers.device)
+def gather_rows(local: torch.Tensor, world: int, group=None, fill=0) -> torch.Tensor:
+    """All-gather of per-rank row blocks [n_r, ...] with unequal n_r, in rank
+    order: pad to the largest block, one all_gather_into_tensor, strip."""
+    n_local = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
     sizes = [torch.zeros_like(n_local) for _ in range(world)]
     dist.all_gather(sizes, n_local, group=group)
     sizes = [int(s.item()) for s in sizes]
     m = max(sizes)
-    pad = torch.full((m,), -1, dtype=local_exit_layers.dtype, device=local_exit_layers.device)
-    pad[: local_exit_layers.numel()] = local_exit_layers
-    out = torch.empty(world * m, dtype=pad.dtype, device=pad.device)
+    pad = torch.full((m,) + tuple(local.shape[1:]), fill, dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    out = torch.empty((world * m,) + tuple(local.shape[1:]), dtype=pad.dtype, device=pad.device)
     dist.all_gather_into_tensor(out, pad, group=group)
     return torch.cat([out[r * m: r * m + sizes[r]] for r in range(world)])
+
+
+def gather_exit_layers(local_exit_layers: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """C1 for unequal shards: pad to the largest shard, all-gather, strip."""
+    return gather_rows(local_exit_layers, world, group, fill=-1)
+
+
+def label_shard(checkpoint_states: dict, final_states, tau: float, world: int, *, group=None,
+                gather: bool = False, labeller=None) -> dict:
+    """Calibration labelling token-sharded over the ranks (BASELINE config 4,
+    ee/calibration.py:201-219): each rank labels its contiguous token shard in
+    one labeller launch; the zero-norm count and the positives of every
+    checkpoint are all-reduced; labels stay sharded (u8 [C, n_local]) unless
+    gather=True (one all-gather, 1 B per token per checkpoint).
+
+    `labeller(checkpoint_states, final_states, tau) -> (layers, sims [C, n],
+    labels u8 [C, n], zero_counts [C])` defaults to the kernel
+    (calibration.label_tensors); the CPU tests pass the oracle."""
+    if labeller is None:
+        from .calibration import label_tensors
+
+        def labeller(cks, fin, t):
+            return label_tensors(cks, fin, t, labels_dtype="u8")
+    layers, sims, labels, zero = labeller(checkpoint_states, final_states, tau)
+    counts = torch.stack([zero.to(torch.int64), labels.to(torch.int64).sum(dim=1)])
+    dist.all_reduce(counts, group=group)
+    out = {"layers": layers, "sims": sims, "labels": labels, "zero_counts": counts[0],
+           "positives": counts[1]}
+    if gather:
+        out["global_labels"] = gather_rows(labels.t().contiguous(), world, group).t()
+    return out

@@ -91,3 +91,55 @@ def test_shard_ranges_cover_exactly():
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             sizes = [b - a for a, b in rs]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _label_worker(rank, world, port, n, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import tide_oracle as O
+        g = np.random.Generator(np.random.PCG64(seed))
+        d = 32
+        fin = g.standard_normal((n, d), dtype=np.float32)
+        cks = {k: (fin + g.standard_normal((n, d), dtype=np.float32) * s).astype(np.float32)
+               for k, s in ((3, 0.1), (7, 0.5), (11, 2.0))}
+        cks[7][::50] = 0.0  # zero-norm rows
+        s0, s1 = S.shard_range(n, rank, world)
+
+        def oracle_labeller(ck, f, tau):
+            lab, sims, _ = O.compute_labels(ck, f, tau)
+            ks = tuple(ck)
+            zero = torch.tensor([int(((np.linalg.norm(ck[k], axis=1) == 0)
+                                      | (np.linalg.norm(f, axis=1) == 0)).sum()) for k in ks])
+            return (ks, torch.from_numpy(np.stack([sims[k] for k in ks])),
+                    torch.from_numpy(np.stack([lab[k] for k in ks]).astype(np.uint8)), zero)
+
+        out = S.label_shard({k: v[s0:s1] for k, v in cks.items()}, fin[s0:s1], 0.9, world,
+                            gather=True, labeller=oracle_labeller)
+        if rank == 0:
+            lab, _, zt = O.compute_labels(cks, fin, 0.9)
+            want = np.stack([lab[k] for k in (3, 7, 11)]).astype(np.uint8)
+            q.put((out["global_labels"].numpy(), want, out["zero_counts"].numpy(),
+                   out["positives"].numpy(), zt))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [999, 1000])
+def test_two_rank_labelling_equals_single_process(n):
+    """Config 4 sharded: gathered labels == the single-process labels; the
+    all-reduced zero-norm and positive counts == the global ones."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_label_worker, args=(r, 2, port, n, 31, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got, want, zero, pos, zt = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_array_equal(got, want)
+    assert int(zero.sum()) == zt
+    np.testing.assert_array_equal(pos, want.sum(axis=1))

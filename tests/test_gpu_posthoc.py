@@ -368,3 +368,35 @@ def test_f32_chain_all_checkpoints_at_once(n, d, L, theta, monkeypatch):
     assert np.array_equal(got, links)
     if theta == 1.0:
         assert np.all(got == P.NO_EXIT)
+
+
+def test_chain_cache_host_inputs_and_router_swap(monkeypatch):
+    """The replay cache with numpy (host) captures — fresh device copies every
+    call, possibly at recycled addresses — and with a router replaced in the
+    bank between calls: always the uncached result."""
+    need_gpu()
+    from paper_2603_21365_b200 import runtime as R
+    ckpts, routers, states, bank, head = _big_case(24, 1024, 600, "bf16", 611, scale=0.2)
+    host = [s.float().cpu().numpy() for s in states]
+    cfg = P.RuntimeConfig(exit_threshold=0.55)
+    R._chain_graphs.entries.clear()
+
+    def uncached(st, bk):
+        monkeypatch.setenv("TIDE_CHAIN_GRAPHS", "0")
+        try:
+            return P.select_exits(st, bk, cfg)
+        finally:
+            monkeypatch.delenv("TIDE_CHAIN_GRAPHS")
+
+    g = np.random.Generator(np.random.PCG64(5))
+    for it in range(4):
+        if it == 2:  # new data in the host arrays
+            for k in ckpts:
+                host[k + 1] = g.standard_normal(host[k + 1].shape).astype(np.float32)
+        assert torch.equal(P.select_exits(host, bank, cfg), uncached(host, bank)), it
+    # replace one router (new object, new weights): a new key, a new recording
+    k0 = ckpts[1]
+    r = O.make_router(1024, 128, k0, g, scale=0.2)
+    bank.routers[k0] = P.Router(layer=k0, w_down=r.w_down, w_up=r.w_up)
+    for it in range(3):
+        assert torch.equal(P.select_exits(states, bank, cfg), uncached(states, bank)), it

@@ -306,12 +306,22 @@ def run_ours(args):
     sustained = ClockSampler(local, period_ms=50)
     sustained.start()
     t_end = time.time() + 0.6
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    sustained_launches = 0
+    s0.record(stream)
     while time.time() < t_end:
         # kernel only: ranks leave this wall-clock loop after different
         # iteration counts, so no collective may be issued in it
         for _ in range(50):
             step(collective=False)
+        sustained_launches += 50
         torch.cuda.synchronize(dev)
+    s1.record(stream)
+    torch.cuda.synchronize(dev)
+    # device time per launch in the power-capped steady state (includes the
+    # host syncs every 50 launches, so a slight overestimate)
+    sustained_ms = s0.elapsed_time(s1) / max(1, sustained_launches)
     barrier()
     clk_sustained = sustained.stop()
     # parity spot-check of the final state on rank 0 (first 2,048 rows vs the oracle)
@@ -398,7 +408,9 @@ def run_ours(args):
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "clocks_sustained": dict(clk_sustained, window="0.6 s of the same step back to back, "
-                                                          "after the timed region"),
+                                                          "after the timed region",
+                                     ms_per_launch=sustained_ms,
+                                     value_per_gpu=N_TOK / (sustained_ms / 1e3)),
             "extra": {"tensor_cores": bool(lib.tide_route_uses_tensor_cores(N.BF16, D, B)),
                       "tflops_tensor": 2.0 * D * B * N_TOK / (kavg / 1e3) / 1e12,
                       "kernel_ms_min": min(kernel_ms), "kernel_ms_max": max(kernel_ms)},

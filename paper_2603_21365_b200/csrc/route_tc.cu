@@ -54,7 +54,7 @@ struct TcParams {
   int64_t n_host;
   const int64_t* n_dev;
   int64_t rows_total;
-  int32_t d, b, npad, bp, tpg, nk, na, nw, nx;
+  int32_t d, b, npad, bp, tpg, nk, na, nw, nx, gran;
   uint32_t idesc, tmem_cols, wslot;
   uint32_t off_a, off_wup, off_bar, off_words, off_ids, off_tmem;
   const int64_t* row_idx;
@@ -92,13 +92,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// Groups are balanced in units of kGran rows (the smallest TMA box of the
-// ragged tail), so per-CTA work differs by at most kGran rows.
+// Groups are balanced in units of p.gran rows: 16 (the smallest TMA box of
+// the ragged tail; per-CTA work differs by at most 16 rows) or, once every
+// CTA holds at least two tiles, 128 — whole tiles per CTA: no MMA on padding
+// rows (a balanced split of 65,536 rows gives every CTA a 59-row fourth tile,
+// 15% of the tensor work on padding) at the price of a one-tile imbalance;
+// measured faster both in the timed region and power-capped.
 constexpr int kGran = 16;
-__device__ __forceinline__ void group_range(int64_t g, int64_t n, int64_t n32, int64_t ng,
-                                            int64_t& r0, int64_t& r1) {
-  r0 = (g * n32 / ng) * kGran;
-  r1 = ((g + 1) * n32 / ng) * kGran;
+constexpr int kBox = 16;  // smallest TMA box of the ragged tail
+__device__ __forceinline__ void group_range(int64_t g, int64_t n, int64_t nu, int64_t ng,
+                                            int gran, int64_t& r0, int64_t& r1) {
+  r0 = (g * nu / ng) * gran;
+  r1 = ((g + 1) * nu / ng) * gran;
   if (r1 > n) r1 = n;
 }
 
@@ -138,9 +143,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (dep_inputs) griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
-  const int64_t n32 = (n + kGran - 1) / kGran;  // number of kGran-row units
+  const int64_t n32 = (n + p.gran - 1) / p.gran;  // number of gran-row units
   const int64_t G = gridDim.x;
-  const int64_t cpg = (int64_t)p.tpg * (128 / kGran);
+  const int64_t cpg = (int64_t)p.tpg * (128 / p.gran);
   int64_t NG = n32 < G ? n32 : G;
   if ((n32 + cpg - 1) / cpg > NG) NG = (n32 + cpg - 1) / cpg;
   const bool gathered = p.row_idx != nullptr;
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     long long pw_cyc = 0, p_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      group_range(g, n, n32, NG, p.gran, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       if (gathered) {
         __syncwarp();
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
             } else {
               // ragged tail: greedy 64/32/16-row boxes (16-row boxes stream poorly)
-              const int rr = (rows_in + kGran - 1) / kGran * kGran;
+              const int rr = (rows_in + kBox - 1) / kBox * kBox;
               mbar_arrive_expect_tx(&a_full[as], (uint32_t)(rr * 128));
               int off = 0;
               if (rr - off >= 64) {
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint64_t desc_hi = sw128_kmajor_desc(0);
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      group_range(g, n, n32, NG, p.gran, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
       tc_fence_after();
@@ -341,7 +346,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     long long sw_cyc = 0, s_begin = pclk();
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      group_range(g, n, n32, NG, p.gran, r0, r1);
       const int T = (int)((r1 - r0 + 127) / 128);
       // sum of squares of this thread's row for each of its two tiles
       // (t = wset, wset + 2), four f32 chains each, from the swizzled A slots
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int gi = 0;
     for (int64_t g = blockIdx.x; g < NG; g += G) {
       int64_t r0, r1;
-      group_range(g, n, n32, NG, r0, r1);
+      group_range(g, n, n32, NG, p.gran, r0, r1);
       const int par = gi & 1;
       mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
@@ -711,16 +716,25 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   if ((rc = make_map(&tm_h128, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
   if ((rc = make_map(&tm_h64, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 64))) return rc;
   if ((rc = make_map(&tm_h32b, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 32))) return rc;
-  if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, kGran))) return rc;
+  if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, kBox))) return rc;
   if ((rc = make_map(&tm_g4, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 1))) return rc;
   if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
 
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = sm_count(dev);
-  const int64_t n32 = (a.n + kGran - 1) / kGran;
+  // whole tiles per CTA once each holds at least two and the row count is
+  // known on the host (a chain link's live count may be far below its
+  // capacity: 16-row units keep every SM busy there); TIDE_K1_GRAN overrides
+  int gran = (a.n_dev == nullptr && a.n >= (int64_t)sms * 256) ? 128 : kGran;
+  {
+    const char* env = getenv("TIDE_K1_GRAN");
+    if (env) gran = atoi(env) == 128 ? 128 : kGran;
+  }
+  p.gran = gran;
+  const int64_t n32 = (a.n + gran - 1) / gran;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n32));
-  if ((n32 + tpg * (128 / kGran) - 1) / (tpg * (128 / kGran)) > kMaxParts / 2)
+  if ((n32 + tpg * (128 / gran) - 1) / (tpg * (128 / gran)) > kMaxParts / 2)
     return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
   static bool attr_set[64] = {false};
   if (!attr_set[dev & 63]) {

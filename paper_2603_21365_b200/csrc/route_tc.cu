@@ -729,7 +729,10 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   int gran = (a.n_dev == nullptr && a.n >= (int64_t)sms * 256) ? 128 : kGran;
   {
     const char* env = getenv("TIDE_K1_GRAN");
-    if (env) gran = atoi(env) == 128 ? 128 : kGran;
+    if (env) {
+      const int v = atoi(env);
+      gran = (v == 32 || v == 64 || v == 128) ? v : kGran;
+    }
   }
   p.gran = gran;
   const int64_t n32 = (a.n + gran - 1) / gran;

@@ -143,3 +143,14 @@ def test_graph_replay_equals_eager(monkeypatch):
     r_e, s_e = T.train_router(x, y, 3, cfg)
     assert np.array_equal(r_g.w_down, r_e.w_down) and np.array_equal(r_g.w_up, r_e.w_up)
     assert s_g == s_e
+
+
+@pytest.mark.parametrize("b1,b2", [(0.9, 0.999), (0.5, 0.95), (0.0, 0.0)])
+def test_bias_correction_table_matches_python_scalars(b1, b2):
+    """The device table holds exactly what the reference's f32 arrays see:
+    f32(1.0 - beta ** t) with Python-float (f64) arithmetic (CPU check)."""
+    cfg = P.CalibrationConfig(adam_beta1=b1, adam_beta2=b2)
+    tab = T._bias_corrections(cfg, 3000)
+    for t in (1, 2, 3, 10, 100, 999, 1000, 2999, 3000):
+        assert tab[t - 1, 0] == np.float32(1.0 - b1 ** t)
+        assert tab[t - 1, 1] == np.float32(1.0 - b2 ** t)

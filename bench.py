@@ -64,8 +64,15 @@ class ClockSampler:
         self.index = index
         self.period_ms = period_ms
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host arrival time, csv line)
         self.thread = None
+        self.window = None  # host-time span of the timed region (mark())
+
+    def mark(self, t0: float, t1: float):
+        """Restrict the summary to samples taken during [t0, t1] (host clock;
+        the nearest samples around it when the region is shorter than the
+        sampling period)."""
+        self.window = (t0, t1)
 
     def start(self):
         try:
@@ -82,7 +89,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -97,7 +104,13 @@ class ClockSampler:
             self.thread.join(timeout=1)
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None and lines:
+            t0, t1 = self.window
+            pad = self.period_ms / 1e3
+            inside = [x for x in lines if t0 <= x[0] <= t1 + pad]
+            lines = inside or [x for x in lines if t0 - 2 * pad <= x[0] <= t1 + 2 * pad] or lines
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -291,11 +304,13 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize(dev)
     launches["n"] = 0
+    w0 = time.time()
     t0.record(stream)
     for i in range(args.steps):
         step()
     t1.record(stream)
     torch.cuda.synchronize(dev)
+    clocks.mark(w0, time.time())
     barrier()
     gpu_launches = launches["n"]
     clk = clocks.stop()
@@ -305,7 +320,8 @@ def run_ours(args):
     # the clocks / throttle reasons under this kernel's load are on record.
     sustained = ClockSampler(local, period_ms=50)
     sustained.start()
-    t_end = time.time() + 0.6
+    ws0 = time.time()
+    t_end = ws0 + 0.6
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
     sustained_launches = 0
@@ -319,6 +335,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
     s1.record(stream)
     torch.cuda.synchronize(dev)
+    sustained.mark(ws0, time.time())
     # device time per launch in the power-capped steady state (includes the
     # host syncs every 50 launches, so a slight overestimate)
     sustained_ms = s0.elapsed_time(s1) / max(1, sustained_launches)

@@ -295,7 +295,7 @@ def run_ours(args):
 
     # the clock sampler starts first so the warm-up launches run right before
     # the timed region (no idle gap for the clocks to drop in)
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, period_ms=20)
     clocks.start()
     for _ in range(args.warmup):
         step()

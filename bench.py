@@ -274,13 +274,17 @@ def run_ours(args):
     ws = Dv.workspace(dev).data_ptr()
     launches = {"n": 0}
 
-    def step(kernel_events=None, collective=True):
+    # Back-to-back steps route the same resident rows: no kernel in flight
+    # writes them, so the launch may start streaming while the previous one
+    # drains (TIDE_ROUTE_INPUTS_READY; the default, flag 0, waits first — its
+    # cost is reported as extra.kernel_ms_inputs_wait).
+    def step(kernel_events=None, collective=True, flags=N.ROUTE_INPUTS_READY):
         if kernel_events is not None:
             kernel_events[0].record(stream)
-        rc = lib.tide_route(h.data_ptr(), D, N_TOK, None, N_TOK, D, N.BF16, None, wd.data_ptr(),
-                            wu.data_ptr(), B, EPS, THETA, 3, scores.data_ptr(), None,
-                            mask.data_ptr(), exit_idx.data_ptr(), cont_idx.data_ptr(), 0, None,
-                            counts.data_ptr(), ws, sh)
+        rc = lib.tide_route_ex(h.data_ptr(), D, N_TOK, None, N_TOK, D, N.BF16, None,
+                               wd.data_ptr(), wu.data_ptr(), B, EPS, THETA, 3, scores.data_ptr(),
+                               None, mask.data_ptr(), exit_idx.data_ptr(), cont_idx.data_ptr(), 0,
+                               None, counts.data_ptr(), ws, flags, sh)
         launches["n"] += 1
         if kernel_events is not None:
             kernel_events[1].record(stream)
@@ -357,6 +361,18 @@ def run_ours(args):
         step(kev[i])
     torch.cuda.synchronize(dev)
     kernel_ms = [a.elapsed_time(b) for a, b in kev]
+    # the same back-to-back region with the default (safe) launch: every
+    # launch waits for the previous grid before reading its rows
+    q0 = torch.cuda.Event(enable_timing=True)
+    q1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        step(collective=False, flags=0)
+    q0.record(stream)
+    for _ in range(args.steps):
+        step(collective=False, flags=0)
+    q1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_wait = q0.elapsed_time(q1) / args.steps
     ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -430,7 +446,8 @@ def run_ours(args):
                                      value_per_gpu=N_TOK / (sustained_ms / 1e3)),
             "extra": {"tensor_cores": bool(lib.tide_route_uses_tensor_cores(N.BF16, D, B)),
                       "tflops_tensor": 2.0 * D * B * N_TOK / (kavg / 1e3) / 1e12,
-                      "kernel_ms_min": min(kernel_ms), "kernel_ms_max": max(kernel_ms)},
+                      "kernel_ms_min": min(kernel_ms), "kernel_ms_max": max(kernel_ms),
+                      "kernel_ms_inputs_wait": ms_wait},
         }
         if not args.no_cpu_baseline and world == 1:  # the host baseline: rank 0 at N = 1
             line["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(

@@ -89,6 +89,27 @@ int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int
                int64_t* counts, void* workspace, void* stream);
 
 /*
+ * tide_route with launch flags.  tide_route(...) == tide_route_ex(..., 0, stream).
+ *
+ * TIDE_ROUTE_INPUTS_READY: the caller asserts that no kernel still in flight
+ * on `stream` writes h, w_down or w_up (e.g. back-to-back routing of one
+ * resident buffer).  The tensor-core kernel is launched with programmatic
+ * dependent launch; by default it executes griddepcontrol.wait before its
+ * first read of h / w_down / w_up, so rows written by the kernel just before
+ * it on the stream (a layer's last kernel in a forward hook, a producer of
+ * the capture) are visible.  With the flag its TMA stream starts while the
+ * previous grid drains; only its writes and look-back wait.  Launches that
+ * read a previous launch's row_idx / n_dev always wait first.
+ */
+#define TIDE_ROUTE_INPUTS_READY 1u
+int tide_route_ex(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev,
+                  int64_t rows_total, int32_t d, int32_t dtype, const int64_t* row_idx,
+                  const void* w_down, const float* w_up, int32_t b, float eps, float theta,
+                  int64_t layer, float* scores, float* logits, uint8_t* mask, int64_t* exit_idx,
+                  int64_t* cont_idx, int32_t ids_from_rows, int64_t* exit_layers,
+                  int64_t* counts, void* workspace, uint32_t flags, void* stream);
+
+/*
  * Stable partition of a u8 mask (ee/router_ops.py:107-154, both strategies —
  * they agree bitwise by contract).  Index outputs as tide_route; when `rows`
  * != NULL also gathers rows (elem_bytes * d bytes each, leading dim ld_rows

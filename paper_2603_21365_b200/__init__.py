@@ -6,6 +6,7 @@ computed by hand-written sm_100a kernels in `_lib/libtide_b200.so` (C ABI:
 include/tide_b200.h).  No CPU fallback.
 """
 
+from ._device import invalidate_device_caches
 from .bank_io import (BadMagicError, BinaryFormatError, ChecksumError, DimensionError,
                       TruncatedError, VersionError, bank_file_size, install_device_weights,
                       load_bank, save_bank)
@@ -34,4 +35,5 @@ __all__ = [
     "TrainingDivergedError",
     "load_bank", "save_bank", "bank_file_size", "install_device_weights", "BinaryFormatError",
     "BadMagicError", "VersionError", "TruncatedError", "ChecksumError", "DimensionError",
+    "invalidate_device_caches",
 ]

@@ -93,3 +93,71 @@ def ptr(t) -> int:
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
+
+
+class IdentityCache:
+    """Bounded LRU of device copies keyed by host-object identity.
+
+    An entry remembers the host objects it was built from through weak
+    references only (so a cached Router / LM head does not pin its host arrays
+    or its device copies for the life of the process once the caller drops
+    it), and a lookup hits only while the very same objects are alive and
+    passed again.  In-place edits of a host array are NOT detected: call
+    `paper_2603_21365_b200.invalidate_device_caches()` after mutating weights
+    in place."""
+
+    def __init__(self, size: int):
+        from collections import OrderedDict
+        self.size = size
+        self._d = OrderedDict()
+        self._lock = threading.Lock()
+
+    @staticmethod
+    def _ref(o):
+        import weakref
+        try:
+            return weakref.ref(o)
+        except TypeError:  # not weak-referenceable (list, tuple): hold it
+            return lambda o=o: o
+
+    def get(self, key, owners):
+        with self._lock:
+            ent = self._d.get(key)
+            if ent is None:
+                return None
+            refs, value = ent
+            if len(refs) != len(owners) or any(r() is not o for r, o in zip(refs, owners)):
+                del self._d[key]
+                return None
+            self._d.move_to_end(key)
+            return value
+
+    def put(self, key, owners, value):
+        with self._lock:
+            self._d[key] = (tuple(self._ref(o) for o in owners), value)
+            self._d.move_to_end(key)
+            while len(self._d) > self.size:
+                self._d.popitem(last=False)
+        return value
+
+    def clear(self):
+        with self._lock:
+            self._d.clear()
+
+    def __len__(self):
+        return len(self._d)
+
+
+_caches: list = []
+
+
+def register_cache(c):
+    _caches.append(c)
+    return c
+
+
+def invalidate_device_caches() -> None:
+    """Drop every cached device copy (router weights, LM heads, decode plans,
+    recorded chain graphs).  Needed after editing host weights in place."""
+    for c in _caches:
+        c.clear()

@@ -19,6 +19,7 @@ MODE_PER_TOKEN, MODE_BATCH_UNANIMOUS = 0, 1
 NO_EXIT = -1
 WORKSPACE_BYTES = 8 << 20
 MAX_DECODE_ROWS = 16
+ROUTE_INPUTS_READY = 1
 
 _c_p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -36,6 +37,9 @@ SIGNATURES = {
     "tide_route": (ctypes.c_int, [_c_p, _i64, _i64, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p,
                                   _i32, _f32, _f32, _i64, _c_p, _c_p, _c_p, _c_p, _c_p, _i32,
                                   _c_p, _c_p, _c_p, _c_p]),
+    "tide_route_ex": (ctypes.c_int, [_c_p, _i64, _i64, _c_p, _i64, _i32, _i32, _c_p, _c_p,
+                                     _c_p, _i32, _f32, _f32, _i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                     _i32, _c_p, _c_p, _c_p, ctypes.c_uint32, _c_p]),
     "tide_compact": (ctypes.c_int, [_c_p, _i64, _c_p, _c_p, _i32, _c_p, _i64, _i32, _i32, _c_p,
                                     _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "tide_exit_project": (ctypes.c_int, [_c_p, _i64, _i32, _c_p, _i64, _c_p, _i32, _c_p, _f32,

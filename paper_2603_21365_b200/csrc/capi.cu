@@ -73,6 +73,17 @@ int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int
                float* scores, float* logits, uint8_t* mask, int64_t* exit_idx,
                int64_t* cont_idx, int32_t ids_from_rows, int64_t* exit_layers,
                int64_t* counts, void* workspace, void* stream) {
+  return tide_route_ex(h, ld_h, n, n_dev, rows_total, d, dtype, row_idx, w_down, w_up, b, eps,
+                       theta, layer, scores, logits, mask, exit_idx, cont_idx, ids_from_rows,
+                       exit_layers, counts, workspace, 0u, stream);
+}
+
+int tide_route_ex(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev,
+                  int64_t rows_total, int32_t d, int32_t dtype, const int64_t* row_idx,
+                  const void* w_down, const float* w_up, int32_t b, float eps, float theta,
+                  int64_t layer, float* scores, float* logits, uint8_t* mask, int64_t* exit_idx,
+                  int64_t* cont_idx, int32_t ids_from_rows, int64_t* exit_layers,
+                  int64_t* counts, void* workspace, uint32_t flags, void* stream) {
   if (d < 1 || b < 1 || n < 0) return set_error(TIDE_ERR_ARG, "tide_route: bad shape");
   if (!w_down || !w_up || !workspace)
     return set_error(TIDE_ERR_ARG, "tide_route: null weights or workspace");
@@ -81,6 +92,8 @@ int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int
   if (dtype != TIDE_F32 && dtype != TIDE_F16 && dtype != TIDE_BF16)
     return set_error(TIDE_ERR_ARG, "tide_route: bad dtype %d", dtype);
   if (row_idx && rows_total < 1) return set_error(TIDE_ERR_ARG, "tide_route: rows_total required");
+  if (flags & ~(uint32_t)TIDE_ROUTE_INPUTS_READY)
+    return set_error(TIDE_ERR_ARG, "tide_route: unknown flags 0x%x", flags);
   if (n == 0 && !n_dev) {
     if (counts)
       if (cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), reinterpret_cast<cudaStream_t>(stream)) !=
@@ -112,20 +125,13 @@ int tide_route(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev, int
   a.exit_layers = exit_layers;
   a.counts = counts;
   a.workspace = workspace;
+  a.flags = flags;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool aligned = ((reinterpret_cast<uintptr_t>(h) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(w_down) & 15) == 0) && (ld_h % 8 == 0);
-  if (route_tc_supported(dtype, d, b) && aligned) {
-    // Single-CTA kernel by default; TIDE_K1_PAIR=1 selects the CTA-pair
-    // (cta_group::2) variant (measured slower so far: DESIGN.md §3).
-    static const char* pair = getenv("TIDE_K1_PAIR");
-    const int npad = (b + 15) / 16 * 16;
-    if (pair && pair[0] == '1' && (npad / 2) % 8 == 0) return route_tc2_launch(a, s);
-    return route_tc_launch(a, s);
-  }
-  // f32 rows: the CUDA-core kernel; the 3xTF32 tensor-core kernel
-  // (route_tf32.cu) only when opted in with TIDE_F32_TC=1 (its accumulation
-  // error exceeds the f32 contract at large d) and 16-byte aligned for TMA
+  if (route_tc_supported(dtype, d, b) && aligned) return route_tc_launch(a, s);
+  // f32 rows: the 3xTF32 tensor-core kernel (route_tf32.cu) where its error
+  // bound holds and the rows are 16-byte aligned for TMA, else CUDA cores
   if (dtype == TIDE_F32 && route_tf32_supported(d, b) && ld_h % 4 == 0 &&
       ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(w_down)) & 15) == 0)
     return route_tf32_launch(a, s);

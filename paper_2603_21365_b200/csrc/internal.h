@@ -33,6 +33,7 @@ struct RouteArgs {
   int64_t* exit_layers;
   int64_t* counts;
   void* workspace;
+  uint32_t flags;  // TIDE_ROUTE_* (tide_route_ex)
 };
 
 int set_error(int code, const char* fmt, ...);
@@ -43,7 +44,6 @@ bool route_tc_supported(int dtype, int d, int b);
 int make_map(CUtensorMap* m, const void* base, int dtype, int64_t cols, int64_t rows,
              int64_t ld_elems, int box_cols, int box_rows);
 extern unsigned long long* g_dbg;
-int route_tc2_launch(const RouteArgs& a, cudaStream_t stream);
 int route_tc_launch(const RouteArgs& a, cudaStream_t stream);
 int route_tcs_plan(const RouteArgs& a, int dev, int* grid);
 int route_tcs_launch(const RouteArgs& a, cudaStream_t stream, int ks, int grid);

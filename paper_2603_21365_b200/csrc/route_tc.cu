@@ -62,6 +62,7 @@ struct TcParams {
   const float* w_up;
   float eps, inv_d, theta;
   int64_t layer;
+  int32_t inputs_ready;  // TIDE_ROUTE_INPUTS_READY
   float* scores;
   float* logits;
   uint8_t* mask;
@@ -139,7 +140,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   // and row index) are read only after it completed; otherwise this grid
   // streams its rows while the previous one finishes its tail, and waits only
   // before its first global write / look-back (epilogue and compaction warps).
-  const bool dep_inputs = p.n_dev != nullptr || p.row_idx != nullptr;
+  // PDL: this grid may be resident before the previous kernel on the stream
+  // has finished; griddepcontrol.wait is what makes that kernel's writes
+  // visible.  Wait before the first read of any input (h, W_down, w_up, the
+  // previous link's live count / row index) unless the caller asserted that
+  // the kernel in flight writes none of them (TIDE_ROUTE_INPUTS_READY and no
+  // row index: back-to-back routing of a resident buffer) — then the stream
+  // starts while the previous grid drains and only the writes wait.
+  const bool dep_inputs = p.n_dev != nullptr || p.row_idx != nullptr || !p.inputs_ready;
   if (dep_inputs) griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
@@ -660,7 +668,7 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   const uint32_t wslot = (uint32_t)npad * 128u;
   int nw = npad <= 128 ? 4 : 3;
   {
-    static const char* env = getenv("TIDE_NW");
+    const char* env = getenv("TIDE_NW");  // read per call
     if (env) nw = std::max(2, std::min(kMaxNW, atoi(env)));
   }
   // smem carve-up (offsets from a 1024-aligned base)
@@ -700,6 +708,7 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.inv_d = (float)(1.0 / (double)a.d);
   p.theta = a.theta;
   p.layer = a.layer;
+  p.inputs_ready = (a.flags & TIDE_ROUTE_INPUTS_READY) ? 1 : 0;
   p.scores = a.scores;
   p.logits = a.logits;
   p.mask = a.mask;
@@ -756,7 +765,7 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   {
-    static const char* env = getenv("TIDE_PDL");
+    const char* env = getenv("TIDE_PDL");  // read per call
     cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
   }
   cfg.attrs = attr;

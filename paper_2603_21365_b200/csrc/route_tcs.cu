@@ -721,7 +721,7 @@ int tcs_launch(const RouteArgs& a, const SplitParams& p, const WMaps<NC>& wm, ui
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   {
-    static const char* env = getenv("TIDE_PDL");
+    const char* env = getenv("TIDE_PDL");  // read per call
     cfg.numAttrs = (env && env[0] == '0') ? 1 : 2;
   }
   cudaError_t e;

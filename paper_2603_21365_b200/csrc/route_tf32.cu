@@ -74,6 +74,7 @@ struct TfParams {
   const float* w_up;
   float eps, inv_d, theta;
   int64_t layer;
+  int32_t inputs_ready;  // TIDE_ROUTE_INPUTS_READY
   float* scores;
   float* logits;
   uint8_t* mask;
@@ -131,7 +132,14 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool dep_inputs = p.n_dev != nullptr || p.row_idx != nullptr;
+  // PDL: this grid may be resident before the previous kernel on the stream
+  // has finished; griddepcontrol.wait is what makes that kernel's writes
+  // visible.  Wait before the first read of any input (h, W_down, w_up, the
+  // previous link's live count / row index) unless the caller asserted that
+  // the kernel in flight writes none of them (TIDE_ROUTE_INPUTS_READY and no
+  // row index: back-to-back routing of a resident buffer) — then the stream
+  // starts while the previous grid drains and only the writes wait.
+  const bool dep_inputs = p.n_dev != nullptr || p.row_idx != nullptr || !p.inputs_ready;
   if (dep_inputs) griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
@@ -563,6 +571,7 @@ int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
   p.inv_d = (float)(1.0 / (double)a.d);
   p.theta = a.theta;
   p.layer = a.layer;
+  p.inputs_ready = (a.flags & TIDE_ROUTE_INPUTS_READY) ? 1 : 0;
   p.scores = a.scores;
   p.logits = a.logits;
   p.mask = a.mask;
@@ -604,7 +613,7 @@ int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   {
-    static const char* env = getenv("TIDE_PDL");
+    const char* env = getenv("TIDE_PDL");  // read per call
     cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
   }
   cfg.attrs = attr;

@@ -105,10 +105,19 @@ class CheckpointCapture:
                 self._route_online(k, rows)
         return fn
 
+    def _new_forward(self, module, inputs):
+        """Forward pre-hook of the first decoder layer: every forward (a
+        generate loop's prefill, then each decode step) starts a new capture
+        and a new peeling chain sized from its own row count."""
+        self._caps.clear()
+        self.exit_layers = None
+        self._chain = None
+
     def __enter__(self):
         self._caps.clear()
         self.exit_layers = None
         self._chain = None
+        self._handles.append(self.layers[0].register_forward_pre_hook(self._new_forward))
         want = set(self.checkpoints) | {self.L - 1}
         for k in sorted(want):
             self._handles.append(self.layers[k].register_forward_hook(self._hook(k)))

@@ -58,19 +58,23 @@ class Router:
         return self.w_down.size + self.w_up.size
 
 
-_weight_cache: dict = {}
+# device copies of router weights: bounded, identity-checked, weak on the host side
+_weight_cache = D.register_cache(D.IdentityCache(256))
 
 
 def device_weights(router, dtype_code: int, device) -> tuple:
     """(w_down [b, d] in the kernel dtype, w_up [b] f32) on `device`, cached.
 
-    Accepts this package's Router or the reference's (duck-typed)."""
+    Accepts this package's Router or the reference's (duck-typed).  A cache
+    hit needs the same router object holding the same w_down / w_up arrays;
+    in-place edits need `invalidate_device_caches()`."""
     dev = torch.device(device)
     wd_host, wu_host = router.w_down, router.w_up
     key = (id(router), dev.index, dtype_code)
-    hit = _weight_cache.get(key)
-    if hit is not None and hit[0] is wd_host and hit[1] is wu_host:
-        return hit[2], hit[3]
+    owners = (router, wd_host, wu_host)
+    hit = _weight_cache.get(key, owners)
+    if hit is not None:
+        return hit
     wd32 = torch.from_numpy(np.ascontiguousarray(wd_host, dtype=np.float32)).to(dev)
     if dtype_code == N.BF16:
         wd = wd32.to(torch.bfloat16)
@@ -79,15 +83,14 @@ def device_weights(router, dtype_code: int, device) -> tuple:
     else:
         wd = wd32
     wu = torch.from_numpy(np.ascontiguousarray(wu_host, dtype=np.float32).reshape(-1)).to(dev)
-    _weight_cache[key] = (wd_host, wu_host, wd.contiguous(), wu.contiguous(), router)
-    return _weight_cache[key][2], _weight_cache[key][3]
+    return _weight_cache.put(key, owners, (wd.contiguous(), wu.contiguous()))
 
 
 def install_cached(router, dtype_code: int, device, wd: torch.Tensor, wu: torch.Tensor) -> None:
     """Seed the device weight cache with copies made elsewhere (bank_io)."""
     dev = torch.device(device)
-    _weight_cache[(id(router), dev.index, dtype_code)] = (
-        router.w_down, router.w_up, wd.contiguous(), wu.reshape(-1).contiguous(), router)
+    _weight_cache.put((id(router), dev.index, dtype_code), (router, router.w_down, router.w_up),
+                      (wd.contiguous(), wu.reshape(-1).contiguous()))
 
 
 def _rows_for(h, router):

@@ -110,19 +110,20 @@ class OutputHead:
         return self
 
 
-_head_cache: dict = {}
+# LM heads can be GBs: a handful of entries, weak on the host objects
+_head_cache = D.register_cache(D.IdentityCache(4))
 
 
 def _device_head(model, dev):
     key = (id(model), dev.index)
     fn, lm = model.final_norm, model.lm_head
-    hit = _head_cache.get(key)
-    if hit is not None and hit[0] is fn and hit[1] is lm:
-        return hit[2], hit[3]
+    owners = (model, fn, lm)
+    hit = _head_cache.get(key, owners)
+    if hit is not None:
+        return hit
     g = D.to_device_f32(fn, dev).reshape(-1)
     w = D.to_device_f32(lm, dev)
-    _head_cache[key] = (fn, lm, g, w, model)
-    return g, w
+    return _head_cache.put(key, owners, (g, w))
 
 
 def _check_bank(model, hidden_states, bank) -> None:
@@ -153,6 +154,7 @@ def _stage_layers(hidden_states, needed: Sequence[int]):
         fast[i] = h
     else:
         if dt in (torch.float32, torch.float16, torch.bfloat16):
+            _check_same_shape(fast, needed)
             return fast, fast[needed[0]].device
     dev = None
     for h in hidden_states:
@@ -173,22 +175,44 @@ def _stage_layers(hidden_states, needed: Sequence[int]):
         if t.dim() != 2:
             raise ValueError(f"hidden state {i} must be [n, d], got {tuple(t.shape)}")
         out[i] = t.contiguous()
+    _check_same_shape(out, needed)
     return out, dev
 
 
-_decode_plans: dict = {}
+def _check_same_shape(staged, needed) -> None:
+    """Every kernel reads each capture with the final capture's n, d and ld,
+    so a shorter or narrower checkpoint tensor would be read out of bounds;
+    the reference fails on it too (ee/runtime.py:166-178 indexes every
+    capture with the final batch's row ids: IndexError / ValueError)."""
+    ref_i = needed[-1]
+    want = tuple(staged[ref_i].shape)
+    for i in needed:
+        got = tuple(staged[i].shape)
+        if got != want:
+            raise ValueError(f"hidden state {i} has shape {got}, expected {want} "
+                             f"(the shape of hidden state {ref_i})")
+
+
+_decode_plans = D.register_cache(D.IdentityCache(32))
+
+# limits of the one-launch decode kernel (decode.cu kDMaxC / kDMaxB); other
+# shapes take the per-checkpoint chain
+MAX_DECODE_CKPTS = 64
+MAX_DECODE_B = 256
+MAX_TAIL_CKPTS = 32  # route_simt.cu kSimtTailC / route_tcs.cu kMaxTailC
 
 
 def _decode_plan(bank, ckpts, code, dev):
-    """ctypes argument arrays of the decode launch (weight pointers, layers),
-    cached per (bank, checkpoints, dtype, device); rebuilt when a router or its
-    weights are replaced."""
+    """ctypes argument arrays of the decode launch (weight pointers, layers)
+    and the device tensors they point into, cached per (bank, checkpoints,
+    dtype, device); rebuilt when a router or its weights are replaced.  The
+    caller keeps the returned tuple alive as long as it uses the pointers."""
     routers = [bank.routers[k] for k in ckpts]
     key = (id(bank), tuple(ckpts), code, dev.index)
-    hit = _decode_plans.get(key)
-    if hit is not None and all(r is h and r.w_down is wd and r.w_up is wu
-                               for r, (h, wd, wu) in zip(routers, hit[0])):
-        return hit[1]
+    owners = (bank, *routers, *(r.w_down for r in routers), *(r.w_up for r in routers))
+    hit = _decode_plans.get(key, owners)
+    if hit is not None:
+        return hit
     ws_w = [device_weights(r, code, dev) for r in routers]
     # W of all checkpoints stacked [C, b, d]: the decode kernel then loads its
     # slices with one TMA tensor map (tide_route_decode detects the layout)
@@ -197,8 +221,14 @@ def _decode_plan(bank, ckpts, code, dev):
     base = stacked.data_ptr()
     arrays = (N.ptr_array([base + i * step for i in range(len(routers))]),
               N.ptr_array([u.data_ptr() for _, u in ws_w]), N.i64_array(ckpts))
-    _decode_plans[key] = ([(r, r.w_down, r.w_up) for r in routers], arrays, (ws_w, stacked), bank)
-    return arrays
+    return _decode_plans.put(key, owners, arrays + ((ws_w, stacked),))
+
+
+def _decode_ok(n, d, code, b, ckpts, staged) -> bool:
+    vec = 4 if code == N.F32 else 8
+    return (0 < n <= N.MAX_DECODE_ROWS and 1 <= len(ckpts) <= MAX_DECODE_CKPTS
+            and b <= MAX_DECODE_B and d % vec == 0
+            and all(staged[k + 1].data_ptr() % 16 == 0 for k in ckpts))
 
 
 class _ChainGraphs:
@@ -237,11 +267,24 @@ class _ChainGraphs:
         st = self.streams.get(dev.index)
         if st is None:
             st = self.streams[dev.index] = torch.cuda.Stream(dev)
-            D.workspace(dev, st.cuda_stream)  # allocated outside any capture
         return st
 
+    @staticmethod
+    def workspace(dev) -> torch.Tensor:
+        """A look-back workspace owned by ONE recorded graph.  Graphs recorded
+        for different caller streams may replay concurrently; a workspace may
+        only be shared by launches that are stream-ordered (common.cuh), so
+        every graph gets its own (allocated and zeroed outside the capture)."""
+        ws = torch.empty(N.WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
+        N.check(N.load().tide_workspace_init(ws.data_ptr(), D.stream_handle(dev)),
+                "tide_workspace_init")
+        return ws
 
-_chain_graphs = _ChainGraphs()
+    def clear(self):
+        self.entries.clear()
+
+
+_chain_graphs = D.register_cache(_ChainGraphs())
 
 
 def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
@@ -253,7 +296,9 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
         staged, dev = _stage_layers(hidden_states, [k + 1 for k in ckpts] + [L])
     final = staged[L]
     n = final.shape[0]
-    if 0 < n <= N.MAX_DECODE_ROWS and ckpts:
+    code = D.dtype_code(final)
+    b = _bottleneck(bank, ckpts)
+    if ckpts and _decode_ok(n, final.shape[1], code, b, ckpts, staged):
         # decode step: the bound launch of these buffers / routers / config,
         # built once (the argument block of tide_route_decode minus the
         # output pointer), then one ctypes call per step
@@ -261,21 +306,18 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
         routers = [bank.routers[k] for k in ckpts]
         key = (id(bank), tuple(ckpts), float(config.exit_threshold), config.mode,
                config.k_min, final.dtype, tuple(final.shape), s,
-               tuple(staged[k + 1].data_ptr() for k in ckpts),
-               tuple((id(r), id(r.w_down), id(r.w_up)) for r in routers))
-        hit = _decode_calls.get(key)
+               tuple(staged[k + 1].data_ptr() for k in ckpts))
+        owners = (bank, *routers, *(r.w_down for r in routers), *(r.w_up for r in routers))
+        hit = _decode_calls.get(key, owners)
         if hit is None:
-            hit = _bind_decode(staged, bank, config, ckpts, dev, s, routers)
-            if len(_decode_calls) >= 64:
-                _decode_calls.clear()
-            _decode_calls[key] = hit
-        if hit[0] is not None:
-            out = torch.empty((n,), dtype=torch.int64, device=dev)
-            args = hit[0]
-            rc = hit[1](*args[:16], out.data_ptr(), *args[17:])
-            if rc:
-                N.check(rc, "tide_route_decode")
-            return out
+            hit = _decode_calls.put(key, owners, _bind_decode(staged, bank, config, ckpts, dev,
+                                                              s))
+        out = torch.empty((n,), dtype=torch.int64, device=dev)
+        args = hit[0]
+        rc = hit[1](*args[:16], out.data_ptr(), *args[17:])
+        if rc:
+            N.check(rc, "tide_route_decode")
+        return out
     if (config.mode == PER_TOKEN and n > N.MAX_DECODE_ROWS and len(ckpts) > 1
             and _ChainGraphs.enabled() and not torch.cuda.is_current_stream_capturing()):
         routers = [bank.routers[k] for k in ckpts]
@@ -295,47 +337,54 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
             while len(cache) > _chain_graphs.size:
                 cache.popitem(last=False)
         elif ent[1] is None:
-            # second call with these buffers: record the chain, then replay it
+            # second call with these buffers: record the chain (with its own
+            # look-back workspace), then replay it
             g = torch.cuda.CUDAGraph()
             st = _chain_graphs.stream(dev)
+            gws = _ChainGraphs.workspace(dev)
             st.wait_stream(torch.cuda.current_stream(dev))
             try:
                 with torch.cuda.graph(g, stream=st):
-                    out = _select_exits_chain(staged, bank, config, ckpts, dev)
+                    out = _select_exits_chain(staged, bank, config, ckpts, dev, ws=gws)
             except Exception:  # not capturable here: stay eager for this key
                 ent[1] = False
                 torch.cuda.synchronize(dev)
                 return _select_exits_chain(staged, bank, config, ckpts, dev)
             ent[1], ent[2] = g, out
+            ent[3] = (bank, routers, gws)
             g.replay()
             return out.clone()
     return _select_exits_chain(staged, bank, config, ckpts, dev)
 
 
-_decode_calls: dict = {}
+_decode_calls = D.register_cache(D.IdentityCache(64))
 
 
-def _bind_decode(staged, bank, config, ckpts, dev, s, routers):
-    """(argument tuple, C function) of the decode launch, or (None, None) when
-    the shape takes the chain path (misaligned rows / width)."""
+def _bottleneck(bank, ckpts) -> int:
+    if hasattr(bank, "bottleneck"):
+        return bank.bottleneck
+    return bank.routers[ckpts[0]].bottleneck if ckpts else 0
+
+
+def _bind_decode(staged, bank, config, ckpts, dev, s):
+    """(argument tuple, C function, plan keep-alive) of the decode launch
+    (the caller checked _decode_ok)."""
     final = staged[bank.num_layers]
     n, d = final.shape
     code = D.dtype_code(final)
-    vec = 4 if code == N.F32 else 8
-    if d % vec or any(staged[k + 1].data_ptr() % 16 for k in ckpts):
-        return (None, None, routers)
-    w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)
-    b = bank.bottleneck if hasattr(bank, "bottleneck") else routers[0].bottleneck
+    plan = _decode_plan(bank, ckpts, code, dev)
+    w_arr, u_arr, l_arr = plan[:3]
+    b = _bottleneck(bank, ckpts)
     mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
     args = (N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
             w_arr, u_arr, b, l_arr, float(np.float32(bank.eps)),
             float(np.float32(config.exit_threshold)), int(config.k_min), mode, None, None,
             0, None, D.workspace(dev, s).data_ptr(), s)
-    # keep the routers alive with the entry so their ids stay unique
-    return (args, N.load().tide_route_decode, routers)
+    # the plan (device weight copies the pointers refer to) lives with the entry
+    return (args, N.load().tide_route_decode, plan)
 
 
-def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev):
+def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None):
     L = bank.num_layers
     final = staged[L]
     n, d = final.shape
@@ -343,15 +392,13 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev):
         return torch.full((n,), NO_EXIT, dtype=torch.int64, device=dev)
     lib = N.load()
     s = D.stream_handle(dev)
-    ws = D.workspace(dev, s).data_ptr()
+    ws = (D.workspace(dev, s) if ws is None else ws).data_ptr()
     theta = float(np.float32(config.exit_threshold))
     eps = float(np.float32(bank.eps))
     code = D.dtype_code(final)
-    b = bank.bottleneck if hasattr(bank, "bottleneck") else bank.routers[ckpts[0]].bottleneck
-    vec = 4 if code == N.F32 else 8
-    decode_ok = d % vec == 0 and all(staged[k + 1].data_ptr() % 16 == 0 for k in ckpts)
-    if n <= N.MAX_DECODE_ROWS and decode_ok:
-        w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)
+    b = _bottleneck(bank, ckpts)
+    if _decode_ok(n, d, code, b, ckpts, staged):
+        w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)[:3]
         mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
         out = torch.empty((n,), dtype=torch.int64, device=dev)  # the kernel writes every row
         N.check(lib.tide_route_decode(
@@ -372,7 +419,8 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev):
                 exit_layers.fill_(k)
                 break
         return exit_layers
-    if code == N.F32 and len(ckpts) >= 2 and n <= _f32_tail_rows() and _tail_enabled():
+    if (code == N.F32 and 2 <= len(ckpts) <= MAX_TAIL_CKPTS and n <= _f32_tail_rows()
+            and d % 4 == 0 and _tail_enabled()):
         # f32 rows, few of them: each CUDA-core link costs its full latency
         # whatever its row count, so score every checkpoint for every row in
         # ONE launch and resolve the first firing one (same map as peeling:
@@ -382,13 +430,14 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev):
         n_t = torch.full((1,), n, dtype=torch.int64, device=dev)
         scratch = torch.empty(len(ckpts) * n, dtype=torch.float32, device=dev)
         tail_count = torch.empty(1, dtype=torch.int64, device=dev)
-        N.check(lib.tide_route_tail(
+        rc = lib.tide_route_tail(
             N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
             every.data_ptr(), n_t.data_ptr(), n, n, N.ptr_array([w.data_ptr() for w, _ in wts]),
             N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(ckpts), eps, theta,
-            scratch.data_ptr(), exit_layers.data_ptr(), tail_count.data_ptr(), 0, ws, s),
-            "tide_route_tail")
-        return exit_layers
+            scratch.data_ptr(), exit_layers.data_ptr(), tail_count.data_ptr(), 0, ws, s)
+        if rc == 0:
+            return exit_layers
+        # a shape the one-launch tail does not take: the per-checkpoint links below
     rem = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
     cnt = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(2)]
     row_idx, n_dev = 0, 0
@@ -494,19 +543,20 @@ class DecodeStep:
         n, d = staged[L].shape
         code = D.dtype_code(staged[L])
         vec = 4 if code == N.F32 else 8
-        if not (1 <= n <= N.MAX_DECODE_ROWS) or d % vec or any(
-                staged[k + 1].data_ptr() % 16 for k in ckpts):
-            raise ValueError(f"DecodeStep needs 1..{N.MAX_DECODE_ROWS} rows, d % {vec} == 0 "
-                             "and 16-byte aligned captures")
+        b = _bottleneck(bank, ckpts)
+        if not _decode_ok(n, d, code, b, ckpts, staged):
+            raise ValueError(f"DecodeStep needs 1..{N.MAX_DECODE_ROWS} rows, d % {vec} == 0, "
+                             f"at most {MAX_DECODE_CKPTS} checkpoints, bottleneck <= "
+                             f"{MAX_DECODE_B} and 16-byte aligned captures")
         if any(staged[k + 1] is not hidden_states[k + 1] for k in ckpts):
             raise ValueError("DecodeStep needs the captures as contiguous CUDA tensors of one "
                              "dtype (a converted copy would not see later writes)")
         self.out = out if out is not None else torch.empty((n,), dtype=torch.int64, device=dev)
-        w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)
-        b = bank.bottleneck if hasattr(bank, "bottleneck") else bank.routers[ckpts[0]].bottleneck
+        plan = _decode_plan(bank, ckpts, code, dev)
+        w_arr, u_arr, l_arr = plan[:3]
         s = D.stream_handle(dev)
         mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
-        self._keep = (staged, w_arr, u_arr, l_arr, bank)
+        self._keep = (staged, plan, bank)
         self._fn = N.load().tide_route_decode
         self._args = (N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n,
                       d, code, w_arr, u_arr, b, l_arr, float(np.float32(bank.eps)),

@@ -5,7 +5,8 @@
 //   select_project  ee/runtime.py:176,180 + ee/model.py:329-338: every row is
 //                   final-normed from the layer it exits at (or the final
 //                   capture), producing the LM-head input in one pass.
-// rmsnorm follows ee/tensor_math.py:35-49 in f32: x / sqrt(sum(x^2)/d + eps) * gain.
+// rmsnorm follows ee/tensor_math.py:35-49 in f32, bit-exactly (numpy's pairwise
+// order for the mean of squares, see np_pairwise_sumsq): x / sqrt(sum(x^2)/d + eps) * gain.
 // One warp per row, 16-byte vector loads, the row held in registers between
 // the two passes when it fits (d <= 32 lanes x 8 x 4 elements).
 #include <cuda_runtime.h>
@@ -19,6 +20,59 @@ namespace tide {
 
 constexpr int kPThreads = 256;
 
+// Sum of squares of one row in numpy's order, so the f32 result is bit-equal
+// to the reference's np.mean(np.square(x), axis=-1) * d (ee/tensor_math.py:43):
+// numpy reduces a contiguous row with FLOAT_pairwise_sum
+// (numpy/_core/src/umath/loops_utils.h.src): n < 8 -> sequential; n <= 128 ->
+// eight strided accumulators r[j] (j, j+8, ...) combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail sequentially;
+// else split at n2 = n/2 - (n/2) % 8 and add the two halves.  Each square is
+// rounded to f32 first (np.square).  Warp-uniform recursion; the leaf's 8
+// chains run on lanes 0-7.  Returns the sum in every lane.
+template <typename T>
+__device__ __forceinline__ float sq_at(const T* a, int i) {
+  const float x = to_f32<T>(a[i]);
+  return __fmul_rn(x, x);
+}
+
+template <typename T>
+__device__ float np_leaf_sumsq(const T* __restrict__ a, int n) {
+  const int lane = threadIdx.x & 31;
+  float res = 0.0f;
+  if (n < 8) {
+    if (lane == 0)
+      for (int i = 0; i < n; ++i) res = __fadd_rn(res, sq_at<T>(a, i));
+  } else {
+    const int body = n - (n % 8);
+    float r = 0.0f;
+    if (lane < 8) {
+      r = sq_at<T>(a, lane);
+      for (int i = 8 + lane; i < body; i += 8) r = __fadd_rn(r, sq_at<T>(a, i));
+    }
+    r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));  // r0+r1, r2+r3, ...
+    r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));  // (r0+r1)+(r2+r3), ...
+    r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));  // both halves
+    if (lane == 0) {
+      res = r;
+      for (int i = body; i < n; ++i) res = __fadd_rn(res, sq_at<T>(a, i));
+    }
+  }
+  return __shfl_sync(0xffffffffu, res, 0);
+}
+
+template <typename T>
+__device__ __noinline__ float np_pairwise_sumsq(const T* __restrict__ a, int n) {
+  if (n <= 128) return np_leaf_sumsq<T>(a, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  const float lo = np_pairwise_sumsq<T>(a, n2);
+  const float hi = np_pairwise_sumsq<T>(a + n2, n - n2);
+  return __fadd_rn(lo, hi);
+}
+
+// rmsnorm of one row (warp): x / sqrt(f32(sum x^2) / f32(d) + eps) * gain with
+// every operation rounded as numpy does it (no FMA contraction): bit-equal to
+// ee/tensor_math.py:35-49 on the f32 (or exactly upcast bf16/f16) row.
 template <typename T>
 __device__ __forceinline__ void norm_row(const T* __restrict__ src, float* __restrict__ dst, int d,
                                          const float* __restrict__ gain, float eps,
@@ -27,23 +81,7 @@ __device__ __forceinline__ void norm_row(const T* __restrict__ src, float* __res
   constexpr int V = 16 / sizeof(T);
   const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (d % V == 0);
-  float ss = 0.f;
-  if (normalize) {
-    if (vec) {
-      for (int k = lane * V; k < d; k += 32 * V) {
-        float f[V];
-        unpack16(*reinterpret_cast<const uint4*>(src + k), f, (const T*)nullptr);
-#pragma unroll
-        for (int e = 0; e < V; ++e) ss = fmaf(f[e], f[e], ss);
-      }
-    } else {
-      for (int k = lane; k < d; k += 32) {
-        const float x = to_f32<T>(src[k]);
-        ss = fmaf(x, x, ss);
-      }
-    }
-    ss = warp_sum_f32(ss);
-  }
+  const float ss = normalize ? np_pairwise_sumsq<T>(src, d) : 0.0f;
   const float den = normalize ? __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps)) : 1.0f;
   if (vec) {
     for (int k = lane * V; k < d; k += 32 * V) {

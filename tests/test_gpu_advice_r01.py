@@ -15,14 +15,14 @@ from oracle import tide_oracle as O
 from tests.gpu_helpers import RTOL, need_gpu
 
 
-def _states_bank(n, d, L, ckpts, seed, dtype=torch.float32, scale=0.2):
+def _states_bank(n, d, L, ckpts, seed, dtype=torch.float32, scale=0.2, interval=1):
     g = np.random.Generator(np.random.PCG64(seed))
     routers = {k: O.make_router(d, 128, k, g, scale=scale) for k in ckpts}
     host = [O.round_to(g.standard_normal((n, d), dtype=np.float32),
                        "f32" if dtype == torch.float32 else "bf16") for _ in range(L + 1)]
     states = [torch.from_numpy(h).cuda().to(dtype) for h in host]
     bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L,
-                       interval=1)
+                       interval=interval)
     return routers, host, states, bank
 
 
@@ -70,7 +70,8 @@ def test_bf16_chain_more_than_32_remaining_checkpoints(monkeypatch):
 @pytest.mark.gpu
 def test_checkpoint_capture_shape_mismatch_raises():
     need_gpu()
-    routers, host, states, bank = _states_bank(64, 128, 12, [3, 7, 11], 4, torch.bfloat16)
+    routers, host, states, bank = _states_bank(64, 128, 12, [3, 7, 11], 4, torch.bfloat16,
+                                               interval=4)
     head = P.OutputHead(12, 128, np.ones(128, np.float32),
                         np.ones((16, 128), np.float32))
     bad = list(states)
@@ -96,8 +97,8 @@ def test_recorded_chain_graphs_own_their_workspace():
     R._chain_graphs.entries.clear()
     n, d, L = 3000, 1024, 24
     ckpts = list(O.checkpoint_layers(L, 4))
-    routers, host, states, bank = _states_bank(n, d, L, ckpts, 12, torch.bfloat16, scale=0.15)
-    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L)
+    routers, host, states, bank = _states_bank(n, d, L, ckpts, 12, torch.bfloat16, scale=0.15,
+                                               interval=4)
     cfg = P.RuntimeConfig(exit_threshold=0.55)
     ref = P.select_exits(states, bank, cfg)
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()

@@ -1,0 +1,2 @@
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider "$@" > gpurun_out/r2_gpu_tests.log 2>&1; echo "tests rc=$?"
+grep -E "passed|failed|FAILED|Error" gpurun_out/r2_gpu_tests.log | tail -30

@@ -203,6 +203,29 @@ int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_
                       int64_t* exit_count, void* workspace, void* stream);
 
 /*
+ * tide_route_decode with the routers' W_down in the packed shared-memory
+ * image made by tide_decode_pack_weights (w_packed, 128-byte aligned; NULL =
+ * tide_route_decode).  The kernel then fetches its W slices with plain 1-D
+ * bulk copies.  Launched with programmatic dependent launch: the W / w_up
+ * fetch overlaps the previous kernel on the stream (the caller's contract:
+ * no kernel in flight writes the router weights); the hidden rows are read
+ * only after it completed.
+ */
+int tide_route_decode_ex(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n, int32_t d,
+                         int32_t dtype, const void* const* w_ptrs, const float* const* wup_ptrs,
+                         int32_t b, const int64_t* layers, float eps, float theta, int64_t k_min,
+                         int32_t mode, float* scores, float* logits, int64_t* exit_layers,
+                         int64_t* exit_count, void* workspace, const void* w_packed, void* stream);
+
+/* Bytes of the packed decode image of C routers ([C][ceil(d/64)][ceil(b/128)] x 16 KB). */
+size_t tide_decode_packed_bytes(int32_t C, int32_t d, int32_t b);
+
+/* Pack C routers' W_down (bf16 / f16 [b, d], HOST array of device pointers)
+ * into the image tide_route_decode_ex reads (out: tide_decode_packed_bytes). */
+int tide_decode_pack_weights(const void* const* w_ptrs, int32_t C, int32_t d, int32_t b,
+                             int32_t dtype, void* out, void* stream);
+
+/*
  * Tail of a per-token peeling chain (ee/runtime.py:166-178) in ONE routing
  * launch: after some links of the chain, the rows still live (row_idx[0 .. *n_dev),
  * device memory, as written by tide_route's cont_idx / counts[1]) are scored

@@ -63,6 +63,13 @@ SIGNATURES = {
                                          ctypes.POINTER(_c_p), ctypes.POINTER(_c_p), _i32,
                                          ctypes.POINTER(_i64), _f32, _f32, _i64, _i32, _c_p,
                                          _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "tide_route_decode_ex": (ctypes.c_int, [ctypes.POINTER(_c_p), _i32, _i64, _i64, _i32, _i32,
+                                            ctypes.POINTER(_c_p), ctypes.POINTER(_c_p), _i32,
+                                            ctypes.POINTER(_i64), _f32, _f32, _i64, _i32, _c_p,
+                                            _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "tide_decode_packed_bytes": (ctypes.c_size_t, [_i32, _i32, _i32]),
+    "tide_decode_pack_weights": (ctypes.c_int, [ctypes.POINTER(_c_p), _i32, _i32, _i32, _i32,
+                                                _c_p, _c_p]),
 }
 
 

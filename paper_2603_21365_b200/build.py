@@ -28,6 +28,11 @@ NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "
            f"-I{os.path.join(ROOT, 'include')}", "--expt-relaxed-constexpr"]
 
 
+def _extra() -> list:
+    """TIDE_NVCC_EXTRA: extra nvcc flags for debug builds (e.g. -DTIDE_DECODE_DEBUG)."""
+    return os.environ.get("TIDE_NVCC_EXTRA", "").split()
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if cand and os.path.exists(cand):
@@ -48,7 +53,7 @@ def _fingerprint() -> str:
                 h.update(f.encode())
                 h.update(fh.read())
     # flags without the absolute include path (the tree is relocated on GPU boxes)
-    h.update(" ".join(ARCH + [f for f in NVFLAGS if not f.startswith("-I")]).encode())
+    h.update(" ".join(ARCH + [f for f in NVFLAGS if not f.startswith("-I")] + _extra()).encode())
     return h.hexdigest()
 
 
@@ -66,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *NVFLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [nvcc, *ARCH, *NVFLAGS, *_extra(), "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")

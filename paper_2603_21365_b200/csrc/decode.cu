@@ -45,6 +45,11 @@ struct DecParams {
   // 128-row block; use_tma = 0 falls back to per-thread cp.async
   CUtensorMap wmap;
   int32_t use_tma;
+  // or (w_packed != NULL) the SW128 shared-memory image of every W, packed
+  // once by tide_decode_pack_weights: [C][nk][MT][128 rows x 128 B]; a CTA's
+  // k-chunks are contiguous 16 KB blocks fetched by plain bulk copies
+  const uint8_t* w_packed;
+  int32_t nk;
   const void* h[kDMaxC];
   const void* w[kDMaxC];
   const float* wup[kDMaxC];
@@ -58,7 +63,7 @@ struct DecParams {
   int64_t* exit_layers;
   int64_t* exit_count;
   Workspace* ws;
-  unsigned long long* dbg;  // optional per-CTA timeline (globaltimer ns), 24 slots per CTA
+  unsigned long long* dbg;  // optional per-CTA timeline (globaltimer ns), 32 slots per CTA (debug)
 };
 
 __device__ __forceinline__ unsigned long long dgt() {
@@ -66,9 +71,21 @@ __device__ __forceinline__ unsigned long long dgt() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define DTL(slot)                                                             \
-  do {                                                                        \
-    if (p.dbg && threadIdx.x == 0) p.dbg[24 * blockIdx.x + (slot)] = dgt();   \
+// Debug timeline (tools/timeline_decode_graph.py): clock64 per phase slot,
+// plus the entry's globaltimer in slot 31; 32 slots per CTA.
+#ifdef TIDE_DECODE_DEBUG
+#define DPR(slot) \
+  do { if (blockIdx.x == 1 && (threadIdx.x == 0 || threadIdx.x == 2)) printf("blk1 t%d at %d\n", threadIdx.x, slot); } while (0)
+#else
+#define DPR(slot) do {} while (0)
+#endif
+#define DTL(slot)                                                                   \
+  do {                                                                              \
+    DPR(slot);                                                                      \
+    if (p.dbg && threadIdx.x == 0) {                                                \
+      p.dbg[32 * blockIdx.x + (slot)] = (unsigned long long)clock64();              \
+      if ((slot) == 0) p.dbg[32 * blockIdx.x + 31] = dgt();                         \
+    }                                                                               \
   } while (0)
 
 __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool ok) {
@@ -157,6 +174,160 @@ __device__ __forceinline__ void decode_finish(const DecParams& p, int c, const f
   DTL(6);
 }
 
+// Step 5 with ONE global round trip (C <= kAtomicMaxC): the CTA holding
+// checkpoint c's row logits writes the scores and adds (1 << 56 | fired << c)
+// to each row's resolution word (per-token) or (1 << 56 | all-fired << c) to
+// the batch word.  The atomic returns the previous value, so the arrival that
+// completes the count already holds every checkpoint's fired bit: it writes
+// the exit layer (first set bit, layers ascending; NO_EXIT if none) and
+// resets the word for the next launch.  Only the fired bits travel through the
+// words (no other data is published), so relaxed atomics suffice.
+constexpr int kAtomicMaxC = 56;
+
+__device__ __forceinline__ unsigned long long atom_add_relaxed_u64(unsigned long long* a,
+                                                                   unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(a), "l"(v) : "memory");
+  return old;
+}
+
+template <int NR>
+__device__ __forceinline__ void decode_finish_atomic(const DecParams& p, int c, const float* sLogit) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp != 0) return;
+  const int n = (int)p.n;
+  const int r = lane;
+  const bool live = r < n;
+  const float t = live ? sLogit[r] : 0.f;
+  // The decision score > theta, where score = f32(sigmoid_f64(t)), from an f32
+  // estimate (|estimate - score| < 4e-7) except within 1e-6 of theta, where
+  // the exact score decides: identical decisions, and the f64 sigmoid for the
+  // score output runs while the resolution atomic is in flight.
+  bool fired = false;
+  if (live && p.layers[c] >= p.k_min) {
+    const float se = sigmoid_f32(t);
+    if (se > p.theta + 1e-6f)
+      fired = true;
+    else if (se >= p.theta - 1e-6f)
+      fired = score_from_logit(t) > p.theta;
+  }
+  DTL(5);
+  constexpr unsigned long long kOne = 1ull << 56, kBits = kOne - 1ull;
+  auto outputs = [&]() {
+    if (live) {
+      if (p.scores) p.scores[(int64_t)c * n + r] = score_from_logit(t);
+      if (p.logits) p.logits[(int64_t)c * n + r] = t;
+    }
+  };
+  if (p.mode == TIDE_MODE_PER_TOKEN) {
+    if (!live) return;
+    const unsigned long long add = kOne | (fired ? (1ull << c) : 0ull);
+    const unsigned long long old = atom_add_relaxed_u64(&p.ws->dec_rows[r], add);
+    outputs();
+    if ((old >> 56) != (unsigned long long)(p.C - 1)) return;
+    const unsigned long long bits = (old + add) & kBits;
+    const int64_t ex = bits ? p.layers[__ffsll((long long)bits) - 1] : (int64_t)TIDE_NO_EXIT;
+    if (p.exit_layers) p.exit_layers[r] = ex;
+    p.ws->dec_rows[r] = 0ull;
+    DTL(6);
+    if (p.exit_count) {
+      const unsigned long long addc = (1ull << 32) | (ex != TIDE_NO_EXIT ? 1ull : 0ull);
+      const unsigned long long oc = atom_add_relaxed_u64(&p.ws->dec_cnt, addc);
+      if ((oc >> 32) == (unsigned long long)(n - 1)) {
+        p.exit_count[0] = (int64_t)((oc + addc) & 0xffffffffull);
+        p.ws->dec_cnt = 0ull;
+      }
+    }
+  } else {
+    const bool all = __all_sync(0xffffffffu, !live || fired);
+    unsigned long long bits = 0ull;
+    int last = 0;
+    if (lane == 0) {
+      const unsigned long long add = kOne | (all ? (1ull << c) : 0ull);
+      const unsigned long long old = atom_add_relaxed_u64(&p.ws->dec_all, add);
+      last = (old >> 56) == (unsigned long long)(p.C - 1);
+      bits = (old + add) & kBits;
+      if (last) p.ws->dec_all = 0ull;
+    }
+    outputs();
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    bits = __shfl_sync(0xffffffffu, bits, 0);
+    const int64_t ex = bits ? p.layers[__ffsll((long long)bits) - 1] : (int64_t)TIDE_NO_EXIT;
+    if (live && p.exit_layers) p.exit_layers[r] = ex;
+    if (lane == 0 && p.exit_count) p.exit_count[0] = ex != TIDE_NO_EXIT ? n : 0;
+  }
+}
+
+// The same resolution for ONE row, by the thread that finished the row's
+// logit t for checkpoint c (cluster kernel: rows are spread over the ranks).
+// Per-token: one atomic on the row's word.  Batch-unanimous: the row's last
+// checkpoint arrival ORs its not-fired mask into dec_all, then counts itself
+// into dec_cnt (release / acquire); the last row reads-and-resets dec_all and
+// writes every row (three round trips, batch mode only).
+__device__ __forceinline__ unsigned long long atom_or_relaxed_u64(unsigned long long* a,
+                                                                  unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.relaxed.gpu.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(a), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long atom_add_acqrel_u64(unsigned long long* a,
+                                                                  unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(a), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long atom_exch_acquire_u64(unsigned long long* a,
+                                                                    unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acquire.gpu.global.exch.b64 %0, [%1], %2;" : "=l"(old) : "l"(a), "l"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void decode_resolve_row(const DecParams& p, int c, int r, float t) {
+  const int n = (int)p.n;
+  bool fired = false;
+  if (p.layers[c] >= p.k_min) {
+    const float se = sigmoid_f32(t);
+    if (se > p.theta + 1e-6f)
+      fired = true;
+    else if (se >= p.theta - 1e-6f)
+      fired = score_from_logit(t) > p.theta;
+  }
+  constexpr unsigned long long kOne = 1ull << 56, kBits = kOne - 1ull;
+  const unsigned long long add = kOne | (fired ? (1ull << c) : 0ull);
+  const unsigned long long old = atom_add_relaxed_u64(&p.ws->dec_rows[r], add);
+  if (p.scores) p.scores[(int64_t)c * n + r] = score_from_logit(t);
+  if (p.logits) p.logits[(int64_t)c * n + r] = t;
+  if ((old >> 56) != (unsigned long long)(p.C - 1)) return;
+  p.ws->dec_rows[r] = 0ull;
+  const unsigned long long bits = (old + add) & kBits;
+  if (p.mode == TIDE_MODE_PER_TOKEN) {
+    const int64_t ex = bits ? p.layers[__ffsll((long long)bits) - 1] : (int64_t)TIDE_NO_EXIT;
+    if (p.exit_layers) p.exit_layers[r] = ex;
+    if (p.exit_count) {
+      const unsigned long long addc = (1ull << 32) | (ex != TIDE_NO_EXIT ? 1ull : 0ull);
+      const unsigned long long oc = atom_add_relaxed_u64(&p.ws->dec_cnt, addc);
+      if ((oc >> 32) == (unsigned long long)(n - 1)) {
+        p.exit_count[0] = (int64_t)((oc + addc) & 0xffffffffull);
+        p.ws->dec_cnt = 0ull;
+      }
+    }
+    return;
+  }
+  const unsigned long long all_c = (p.C >= 64) ? ~0ull : ((1ull << p.C) - 1ull);
+  atom_or_relaxed_u64(&p.ws->dec_all, ~bits & all_c);  // checkpoints where row r did not fire
+  const unsigned long long oc = atom_add_acqrel_u64(&p.ws->dec_cnt, 1ull);
+  if (oc != (unsigned long long)(n - 1)) return;
+  const unsigned long long notfired = atom_exch_acquire_u64(&p.ws->dec_all, 0ull);
+  p.ws->dec_cnt = 0ull;
+  const unsigned long long allbits = ~notfired & all_c;
+  const int64_t ex = allbits ? p.layers[__ffsll((long long)allbits) - 1] : (int64_t)TIDE_NO_EXIT;
+  if (p.exit_layers)
+    for (int i = 0; i < n; ++i) p.exit_layers[i] = ex;
+  if (p.exit_count) p.exit_count[0] = ex != TIDE_NO_EXIT ? n : 0;
+}
+
 // Steps 3-4, shared by both kernels.  sRes [b][NR] + sSS [NR] hold this CTA's
 // partial tile; sWup [b] the checkpoint's w_up; sLog [kDWarps][NR] scratch.
 template <int NR>
@@ -231,7 +402,12 @@ __device__ __forceinline__ void decode_tail(const DecParams& p, int c, int s, fl
     sLog[kDWarps * NR + threadIdx.x] = t;
   }
   __syncthreads();
-  decode_finish<NR>(p, c, sLog + kDWarps * NR, last_s);
+  if (p.C <= kAtomicMaxC) {
+    if (threadIdx.x == 0) p.ws->tickets[c] = 0;  // reset for the next launch (graph replay safe)
+    decode_finish_atomic<NR>(p, c, sLog + kDWarps * NR);
+  } else {
+    decode_finish<NR>(p, c, sLog + kDWarps * NR, last_s);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -264,7 +440,26 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   uint64_t* mma_done = reinterpret_cast<uint64_t*>(sWup + ((b + 1) & ~1));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 1);
   DTL(0);
-  if (kClu) cluster_arrive_relaxed();  // this CTA's smem exists (peers write it after step 3a)
+  if (threadIdx.x == 0) griddep_launch_dependents();
+  // cluster reduction buffers: this CTA's partial tile as row blocks
+  // sRows[r][RB] (RB = b + 4: the row's b partial pre-activations, then its
+  // partial sum of squares), and recv[k][src][RB] for the rows this rank owns
+  // (row r is owned by rank r % S; k = r / S)
+  const int RB = b + 4;
+  uint64_t* recv_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tmem_slot) + 8 + 8 * kDMaxKc);
+  float* sRows = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(tmem_slot) + 16 + 8 * kDMaxKc + 15) & ~(uintptr_t)15);
+  float* recv = sRows + (size_t)NR * RB;
+  const int own_rows = kClu ? (n > s ? (n - s + p.S - 1) / p.S : 0) : 0;  // rows r = s, s + S, ...
+  if (kClu) {
+    if (threadIdx.x == 0 && own_rows > 0) {
+      // armed before the cluster arrive: peers send only after their cluster wait
+      mbar_init(recv_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arrive_expect_tx(recv_bar, (uint32_t)own_rows * (uint32_t)(p.S - 1) * (uint32_t)RB * 4u);
+    }
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+  }
 
   // 1. one round trip: W slice + hidden slice as 16-byte pieces into the
   //    swizzled K-major layout (piece q of row j at ((q ^ (j & 7)) << 4))
@@ -272,19 +467,34 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   const T* H = reinterpret_cast<const T*>(p.h[c]);
   const int per_row = nkc * 8;
   uint64_t* wfull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tmem_slot) + 8);  // [kDMaxKc]
-  if (p.use_tma) {
-    // W slice by TMA, one barrier per k-chunk: the MMAs of early chunks run
-    // while later chunks land
+  // W slices land on ONE barrier (wfull[0]): with PDL they are fetched while
+  // the previous kernel runs, so by the time the rows land W is resident and
+  // a single wait precedes the whole MMA stream (a wait per k-chunk cost
+  // ~500 cycles each, measured).
+  const int nkc_mma = p.w_packed ? min(nkc, p.nk - c0 / 64) : nkc;  // packed: chunks past d skipped
+  if (p.w_packed) {
+    // the pre-swizzled image: one 1-D bulk copy (MT x 16 KB) per k-chunk
     if (threadIdx.x == 0) {
-      for (int kc = 0; kc < nkc; ++kc) mbar_init(&wfull[kc], 1);
+      mbar_init(&wfull[0], 1);
       fence_mbar_init();
       const uint64_t pol = policy_evict_last();  // every decode step re-reads it
-      for (int kc = 0; kc < nkc; ++kc) {
-        mbar_arrive_expect_tx(&wfull[kc], (uint32_t)MT * 16384u);
+      const int kc0 = c0 / 64;
+      const uint32_t bytes = (uint32_t)MT * 16384u;
+      mbar_arrive_expect_tx(&wfull[0], bytes * (uint32_t)nkc_mma);
+      for (int kc = 0; kc < nkc_mma; ++kc)
+        bulk_g2s(sA + (size_t)kc * MT * 16384, p.w_packed + ((size_t)c * p.nk + kc0 + kc) * bytes,
+                 bytes, &wfull[0], pol);
+    }
+  } else if (p.use_tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&wfull[0], 1);
+      fence_mbar_init();
+      const uint64_t pol = policy_evict_last();  // every decode step re-reads it
+      mbar_arrive_expect_tx(&wfull[0], (uint32_t)(nkc * MT) * 16384u);
+      for (int kc = 0; kc < nkc; ++kc)
         for (int mt = 0; mt < MT; ++mt)
-          tma_load_2d(sA + ((size_t)kc * MT + mt) * 16384, &p.wmap, &wfull[kc], c0 + kc * 64,
+          tma_load_2d(sA + ((size_t)kc * MT + mt) * 16384, &p.wmap, &wfull[0], c0 + kc * 64,
                       c * b + mt * 128, pol);
-      }
     }
   } else {
     for (int i = threadIdx.x; i < b * per_row; i += kDThreads) {
@@ -295,13 +505,6 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
       cp_async16_zfill(dst, W + (int64_t)j * p.d + (in ? col : 0), in);
     }
   }
-  for (int i = threadIdx.x; i < 16 * per_row; i += kDThreads) {
-    const int r = i / per_row, rem = i - r * per_row, kc = rem >> 3, q = rem & 7;
-    const int col = c0 + kc * 64 + q * 8;
-    const bool in = col < p.d && r < n;
-    uint8_t* dst = sB + (size_t)kc * 2048 + r * 128 + ((q ^ (r & 7)) << 4);
-    cp_async16_zfill(dst, H + (in ? (int64_t)r * p.ld_h + col : 0), in);
-  }
   for (int j = threadIdx.x; j < b; j += kDThreads) sWup[j] = p.wup[c][j];
   if (threadIdx.x == 0) {
     mbar_init(mma_done, 1);
@@ -311,6 +514,19 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
     tmem_alloc(tmem_slot, 32);
     tmem_relinquish();
   }
+  // PDL: everything above reads only the static router weights (the caller's
+  // contract: no kernel in flight writes W_down / w_up), so it overlaps the
+  // previous kernel on the stream; the hidden rows and the workspace words
+  // are touched only after it completed.
+  griddep_wait();
+  DTL(12);
+  for (int i = threadIdx.x; i < 16 * per_row; i += kDThreads) {
+    const int r = i / per_row, rem = i - r * per_row, kc = rem >> 3, q = rem & 7;
+    const int col = c0 + kc * 64 + q * 8;
+    const bool in = col < p.d && r < n;
+    uint8_t* dst = sB + (size_t)kc * 2048 + r * 128 + ((q ^ (r & 7)) << 4);
+    cp_async16_zfill(dst, H + (in ? (int64_t)r * p.ld_h + col : 0), in);
+  }
   cp_async_wait_all();
   tc_fence_before();
   __syncthreads();
@@ -318,30 +534,30 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   const uint32_t tmem_base = *tmem_slot;
   DTL(1);
 
-  // 2. MMAs (warp 0, one elected lane): D[mt] (128 x 16) += A[kc][mt] . B[kc]^T
+  // 2. MMAs: warp 0 walks the loop (descriptors warp-uniform -> uniform
+  //    registers), one elected lane issues each MMA: D[mt] (128 x 16) +=
+  //    A[kc][mt] . B[kc]^T, ~39 cycles per N = 16 MMA back to back (measured)
   if (warp == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async -> MMA operands
+    if (p.use_tma || p.w_packed) mbar_wait_spin(&wfull[0], 0);
     tc_fence_after();
-    if (elect_one()) {
-      const uint64_t desc_hi = sw128_kmajor_desc(0);
-      const uint32_t idesc = f16_idesc(kBF16 ? 1 : 0, 128, 16);
-      for (int kc = 0; kc < nkc; ++kc) {
-        if (p.use_tma) {
-          mbar_wait(&wfull[kc], 0);
-          tc_fence_after();
-        }
-        for (int mt = 0; mt < MT; ++mt) {
-          const uint64_t ad =
-              desc_hi | (uint64_t)((smem_u32(sA + ((size_t)kc * MT + mt) * 16384) & 0x3FFFFu) >> 4);
-          const uint64_t bd = desc_hi | (uint64_t)((smem_u32(sB + (size_t)kc * 2048) & 0x3FFFFu) >> 4);
+    DTL(8);
+    const uint64_t desc_hi = sw128_kmajor_desc(0);
+    const uint32_t idesc = f16_idesc(kBF16 ? 1 : 0, 128, 16);
+    const uint64_t a_base = desc_hi | (uint64_t)((smem_u32(sA) & 0x3FFFFu) >> 4);
+    const uint64_t b_base = desc_hi | (uint64_t)((smem_u32(sB) & 0x3FFFFu) >> 4);
+    for (int kc = 0; kc < nkc_mma; ++kc)
+      for (int mt = 0; mt < MT; ++mt) {
+        const uint64_t ad = a_base + (uint64_t)(((kc * MT + mt) * 16384) >> 4);
+        const uint64_t bd = b_base + (uint64_t)((kc * 2048) >> 4);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k)
+          if (elect_one())
             tc_mma_f16(tmem_base + (uint32_t)(mt * 16), ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
-        }
       }
-      tc_commit(mma_done);
-    }
+    if (elect_one()) tc_commit(mma_done);
     __syncwarp();
+    DTL(9);
   } else if (warp >= 4) {
     // partial sums of squares of the hidden rows (8 threads per row, fixed order)
     const int t = threadIdx.x - 128, r = t >> 3, q = t & 7;
@@ -357,11 +573,16 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
     ss += __shfl_xor_sync(0xffffffffu, ss, 1);
     ss += __shfl_xor_sync(0xffffffffu, ss, 2);
     ss += __shfl_xor_sync(0xffffffffu, ss, 4);
-    if (r < NR && q == 0) sRes[(size_t)b * NR + r] = ss;
+    if (r < NR && q == 0) {
+      if (kClu)
+        sRows[(size_t)r * RB + b] = ss;
+      else
+        sRes[(size_t)b * NR + r] = ss;
+    }
   }
   // 3a. accumulators -> sRes[j][r] (warps 0-3: TMEM lane quadrant = warp)
   if (warp < 4) {
-    mbar_wait(mma_done, 0);
+    mbar_wait_spin(mma_done, 0);
     tc_fence_after();
     for (int mt = 0; mt < MT; ++mt) {
       uint32_t v[16];
@@ -369,8 +590,13 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
       tmem_ld_wait();
       const int j = mt * 128 + 32 * warp + lane;
       if (j < b) {
+        if (kClu) {
 #pragma unroll
-        for (int r = 0; r < NR; ++r) sRes[(size_t)j * NR + r] = __uint_as_float(v[r]);
+          for (int r = 0; r < NR; ++r) sRows[(size_t)r * RB + j] = __uint_as_float(v[r]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < NR; ++r) sRes[(size_t)j * NR + r] = __uint_as_float(v[r]);
+        }
       }
     }
     tc_fence_before();
@@ -385,57 +611,87 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
     decode_tail<NR>(p, c, s, sRes, sWup, sLog, &last_s);
     return;
   }
-  // 3b. DSMEM reduction.  Rank q owns units [q U, (q+1) U); every CTA stores its
-  // partial of those units into q's recv[src = own rank], and its partial sum
-  // of squares into every CTA's recv_ss[src].
+  // 3b. DSMEM exchange by rows: thread r (< n) ships row r's block (RB
+  //     floats) with one bulk copy to the rank that owns the row (r % S),
+  //     into its slot for this source rank, completing on that rank's
+  //     barrier.  No cluster barrier on the critical path (the wait for every
+  //     rank's start was satisfied during the W / row loads).
   const uint32_t rank = (uint32_t)s;  // cluster dims (S, 1, 1), blockIdx.x = c S + s
-  const int S = p.S, U = (b + S - 1) / S;
-  float* recv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 8 + 8 * kDMaxKc);
-  float* recv_ss = recv + (size_t)S * U * NR;
-  float* plog = recv_ss + (size_t)S * NR;
-  float* yv = plog + (size_t)S * NR;
-  const float* sSS = sRes + (size_t)b * NR;
-  cluster_wait();  // every peer started
-  for (int i = threadIdx.x; i < b * NR; i += kDThreads) {
-    const int j = i / NR, r = i - j * NR;
-    const int q = j / U, uu = j - q * U;
-    st_dsmem_f32(dsmem_addr(smem_u32(recv + ((size_t)rank * U + uu) * NR + r), (uint32_t)q), sRes[i]);
-  }
-  for (int i = threadIdx.x; i < S * NR; i += kDThreads) {
-    const int q = i / NR, r = i - q * NR;
-    st_dsmem_f32(dsmem_addr(smem_u32(recv_ss + rank * NR + r), (uint32_t)q), sSS[r]);
-  }
-  cluster_sync_all();  // release / acquire: every partial landed
-  DTL(3);
-  // 4. this CTA's units: totals over the S slices (fixed order), scale,
-  //    SiLU, w_up; partial logit per row -> rank 0's plog[rank]
-  for (int i = threadIdx.x; i < U * NR; i += kDThreads) {
-    const int uu = i / NR, r = i - uu * NR;
-    const int j = (int)rank * U + uu;
-    float a = 0.f, ss = 0.f;
-    for (int src = 0; src < S; ++src) {
-      a += recv[((size_t)src * U + uu) * NR + r];
-      ss += recv_ss[src * NR + r];
+  const int S = p.S;
+  const uint32_t rb_bytes = (uint32_t)RB * 4u;
+  if (warp == 0) {
+    // the whole warp waits (a partial-warp barrier.cluster.wait never
+    // completed here, measured), then each sending lane issues its copy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // sRows -> bulk copy reads
+    cluster_wait();
+    if (lane < n && (lane % S) != (int)rank) {
+      const int r = lane, q = r % S, k = r / S;
+      const uint32_t dst = dsmem_addr(smem_u32(recv + ((size_t)k * S + rank) * RB), (uint32_t)q);
+      const uint32_t bar = dsmem_addr(smem_u32(recv_bar), (uint32_t)q);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "r"(smem_u32(sRows + (size_t)r * RB)), "r"(rb_bytes), "r"(bar)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // read before exit
     }
-    const float scale = rms_scale(ss, p.inv_d, p.eps);
-    yv[i] = j < b ? __fmul_rn(sWup[j], silu_f32(__fmul_rn(a, scale))) : 0.f;
   }
-  __syncthreads();
-  if (threadIdx.x < NR) {
-    float t = 0.f;
-    for (int uu = 0; uu < U; ++uu) t += yv[uu * NR + threadIdx.x];
-    st_dsmem_f32(dsmem_addr(smem_u32(plog + rank * NR + threadIdx.x), 0u), t);
+  if (own_rows == 0) return;
+#ifdef TIDE_DECODE_DEBUG
+  {
+    uint32_t spins = 0;
+    while (!mbar_try_wait(smem_u32(recv_bar), 0)) {
+      if (++spins == (1u << 22) && threadIdx.x == 0) {
+        unsigned long long st = *reinterpret_cast<volatile unsigned long long*>(recv_bar);
+        uint32_t dyn;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        printf("decode hang: blk %d rank %u own %d n %d S %d RB %d state %llx | bar %u rows %u recv %u "
+               "wup %u tslot %u sA %u sB %u sRes %u dyn %u\n", blockIdx.x, rank, own_rows, n, S, RB, st,
+               smem_u32(recv_bar), smem_u32(sRows), smem_u32(recv), smem_u32(sWup), smem_u32(tmem_slot),
+               smem_u32(sA), smem_u32(sB), smem_u32(sRes), dyn);
+      }
+      if (spins > (1u << 24)) __trap();
+    }
   }
-  cluster_sync_all();  // rank 0 holds every partial logit; no DSMEM traffic after this
-  DTL(4);
-  if (rank != 0) return;
-  if (threadIdx.x < NR) {
-    float t = 0.f;
-    for (int src = 0; src < S; ++src) t += plog[src * NR + threadIdx.x];
-    yv[threadIdx.x] = t;
+#endif
+  mbar_wait_spin(recv_bar, 0);
+  DTL(3);
+  // 4. rows owned here (k = 0 .. own_rows - 1, row r = rank + k S), 128
+  //    threads per row, unit j per thread: totals over the S slices in fixed
+  //    source order, RMS scale, SiLU (tanh form, as K1: logit error <=
+  //    2.5e-4 m), w_up; the row's sum in a fixed tree (lanes, then warps)
+  float* red = sLog;  // [2][4] warp partials
+  for (int kb = 0; kb < own_rows; kb += 2) {  // uniform over the CTA
+    const int k = kb + (threadIdx.x >> 7), jt = threadIdx.x & 127;
+    const int r = (int)rank + k * S;
+    const bool row_ok = k < own_rows && r < n;
+    float y = 0.f;
+    if (row_ok) {
+      float ss = 0.f;
+      for (int src = 0; src < S; ++src)
+        ss += (src == (int)rank) ? sRows[(size_t)r * RB + b] : recv[((size_t)k * S + src) * RB + b];
+      const float hs = 0.5f * rms_scale(ss, p.inv_d, p.eps);
+      for (int j = jt; j < b; j += 128) {
+        float a = 0.f;
+#pragma unroll 4
+        for (int src = 0; src < S; ++src)
+          a += (src == (int)rank) ? sRows[(size_t)r * RB + j] : recv[((size_t)k * S + src) * RB + j];
+        const float h = __fmul_rn(a, hs);
+        y = fmaf(sWup[j], fmaf(h, tanh_approx(h), h), y);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (lane == 0) red[warp] = y;
+    __syncthreads();
+    DTL(4);
+    if (jt == 0 && row_ok) {
+      const int g = threadIdx.x >> 7;
+      const float t = (red[4 * g] + red[4 * g + 1]) + (red[4 * g + 2] + red[4 * g + 3]);
+      decode_resolve_row(p, c, r, t);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  decode_finish<NR>(p, c, yv, &last_s, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -461,10 +717,12 @@ __global__ void __launch_bounds__(kDThreads) decode_f32_kernel(const __grid_cons
   DTL(0);
   const T* W = reinterpret_cast<const T*>(p.w[c]);
   const T* H = reinterpret_cast<const T*>(p.h[c]);
+  if (threadIdx.x == 0) griddep_launch_dependents();
   for (int i = threadIdx.x; i < b * nch; i += kDThreads) {
     const int j = i / nch, k = i - j * nch;
     cp_async16_zfill(sW + (size_t)j * p.cs + k * V, W + (int64_t)j * p.d + c0 + k * V, true);
   }
+  griddep_wait();  // PDL: the rows (and the workspace) only after the previous kernel
   for (int i = threadIdx.x; i < NR * nch; i += kDThreads) {
     const int r = i / nch, k = i - r * nch;
     cp_async16_zfill(sH + (size_t)r * p.cs + k * V, H + (int64_t)(r < n ? r : 0) * p.ld_h + c0 + k * V,
@@ -542,15 +800,19 @@ size_t smem_tc(int b, int cs, int NR) {
   const int MT = (b + 127) / 128, nkc = cs / 64;
   return 1024 + (size_t)nkc * MT * 16384 + (size_t)nkc * 2048 + tail_bytes(b, NR) + 32 + 8 * kDMaxKc;
 }
-// extra smem of the cluster variant: recv [S][U][NR] + recv_ss [S][NR] + plog [S][NR] + yv [U][NR]
+// extra smem of the cluster variant: sRows [NR][b + 4] + recv [ceil(NR/S)][S][b + 4] (+ alignment)
 size_t smem_clu(int b, int S, int NR) {
-  const int U = (b + S - 1) / S;
-  return 16 + ((size_t)S * U * NR + 2 * (size_t)S * NR + (size_t)U * NR) * 4;
+  return 32 + ((size_t)NR + (size_t)((NR + S - 1) / S) * S) * (size_t)(b + 4) * 4;
 }
 size_t smem_f32(int b, int cs, int NR) { return (size_t)(b + NR) * cs * 4 + tail_bytes(b, NR); }
 
 // Largest-cluster plan: clusters of S slice-CTAs (one per checkpoint) when all
 // C of them can be co-resident; else 0 (the global-ticket reduction).
+bool pdl_enabled() {
+  const char* env = getenv("TIDE_PDL");  // read per call
+  return !(env && env[0] == '0');
+}
+
 template <typename K>
 int launch_cluster(K kernel, const DecParams& p, size_t smem, cudaStream_t s) {
   // co-resident cluster counts per (kernel, S, smem), queried once each
@@ -567,13 +829,15 @@ int launch_cluster(K kernel, const DecParams& p, size_t smem, cudaStream_t s) {
   cfg.blockDim = dim3(kDThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute a[1];
+  cudaLaunchAttribute a[2];
   a[0].id = cudaLaunchAttributeClusterDimension;
   a[0].val.clusterDim.x = (unsigned)p.S;
   a[0].val.clusterDim.y = 1;
   a[0].val.clusterDim.z = 1;
+  a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = a;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1;  // occupancy query without PDL
   int ok_for = -1;
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -612,6 +876,7 @@ int launch_cluster(K kernel, const DecParams& p, size_t smem, cudaStream_t s) {
   // a straggler wave costs more than a narrower split (measured: 16-CTA
   // clusters with 7 of 9 resident 11.0 us vs 8-CTA clusters all resident 10.1)
   if (ok_for < p.C) return 1;  // caller tries the next split / falls back
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaLaunchKernelEx(&cfg, kernel, p);
   return check_launch("decode_tc_kernel (cluster)") == TIDE_OK ? 0 : -1;
 }
@@ -623,13 +888,75 @@ int launch_kernel(K kernel, const DecParams& p, size_t smem, cudaStream_t s, siz
       return check_launch("decode_kernel smem attribute");
     *attr = smem;
   }
-  kernel<<<p.C * p.S, kDThreads, smem, s>>>(p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.C * p.S));
+  cfg.blockDim = dim3(kDThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, p);
   return check_launch("decode_kernel");
+}
+
+// The SW128 K-major shared-memory image of every router's W (bf16 / f16):
+// block (c, kc, mt) = rows mt*128 .. +127 of W_c, columns kc*64 .. +63, 16-byte
+// piece q of row j at j*128 + ((q ^ (j & 7)) << 4); zero past b / d.
+__global__ void decode_pack_kernel(const __grid_constant__ DecParams p, uint8_t* out, int MT) {
+  const int64_t pieces = (int64_t)p.C * p.nk * MT * 128 * 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pieces;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i & 7);
+    const int j = (int)((i >> 3) & 127);
+    int64_t blk = i >> 10;  // (c, kc, mt)
+    const int mt = (int)(blk % MT);
+    blk /= MT;
+    const int kc = (int)(blk % p.nk);
+    const int c = (int)(blk / p.nk);
+    const int row = mt * 128 + j, col = kc * 64 + q * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (row < p.b && col < p.d)
+      v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.w[c]) +
+                                          (int64_t)row * p.d + col);
+    *reinterpret_cast<uint4*>(out + (((int64_t)c * p.nk + kc) * MT + mt) * 16384 + j * 128 +
+                              ((q ^ (j & 7)) << 4)) = v;
+  }
 }
 
 }  // namespace
 
 }  // namespace tide
+
+extern "C" size_t tide_decode_packed_bytes(int32_t C, int32_t d, int32_t b) {
+  if (C < 1 || d < 1 || b < 1) return 0;
+  return (size_t)C * ((d + 63) / 64) * ((b + 127) / 128) * 16384u;
+}
+
+extern "C" int tide_decode_pack_weights(const void* const* w_ptrs, int32_t C, int32_t d, int32_t b,
+                                        int32_t dtype, void* out, void* stream) {
+  using namespace tide;
+  if (C < 1 || C > kDMaxC || d < 8 || d % 8 || b < 1 || b > kDMaxB || !out || !w_ptrs)
+    return set_error(TIDE_ERR_ARG, "tide_decode_pack_weights: bad arguments");
+  if (dtype != TIDE_BF16 && dtype != TIDE_F16)
+    return set_error(TIDE_ERR_UNSUPPORTED, "tide_decode_pack_weights: bf16 / f16 only");
+  DecParams p{};
+  for (int c = 0; c < C; ++c) {
+    if (!w_ptrs[c] || (reinterpret_cast<uintptr_t>(w_ptrs[c]) & 15))
+      return set_error(TIDE_ERR_ARG, "tide_decode_pack_weights: unaligned weights");
+    p.w[c] = w_ptrs[c];
+  }
+  p.C = C;
+  p.d = d;
+  p.b = b;
+  p.nk = (d + 63) / 64;
+  const int MT = (b + 127) / 128;
+  decode_pack_kernel<<<296, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      p, reinterpret_cast<uint8_t*>(out), MT);
+  return check_launch("decode_pack_kernel");
+}
 
 extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n,
                                  int32_t d, int32_t dtype, const void* const* w_ptrs,
@@ -637,6 +964,18 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
                                  float eps, float theta, int64_t k_min, int32_t mode,
                                  float* scores, float* logits, int64_t* exit_layers,
                                  int64_t* exit_count, void* workspace, void* stream) {
+  return tide_route_decode_ex(h_ptrs, C, ld_h, n, d, dtype, w_ptrs, wup_ptrs, b, layers, eps,
+                              theta, k_min, mode, scores, logits, exit_layers, exit_count,
+                              workspace, nullptr, stream);
+}
+
+extern "C" int tide_route_decode_ex(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n,
+                                 int32_t d, int32_t dtype, const void* const* w_ptrs,
+                                 const float* const* wup_ptrs, int32_t b, const int64_t* layers,
+                                 float eps, float theta, int64_t k_min, int32_t mode,
+                                 float* scores, float* logits, int64_t* exit_layers,
+                                 int64_t* exit_count, void* workspace, const void* w_packed,
+                                 void* stream) {
   using namespace tide;
   if (C < 1 || C > kDMaxC) return set_error(TIDE_ERR_ARG, "C must be in [1, %d]", kDMaxC);
   if (n < 1 || n > kDMaxRows) return set_error(TIDE_ERR_ARG, "decode rows must be in [1, %d]", kDMaxRows);
@@ -691,9 +1030,21 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
   p.exit_count = exit_count;
   p.ws = reinterpret_cast<Workspace*>(workspace);
   p.dbg = g_dbg;
-  // stacked W ([C, b, d] contiguous, the runtime's decode plan) -> one tensor map
+  // packed W image (tide_decode_pack_weights) -> 1-D bulk copies; else
+  // stacked W ([C, b, d] contiguous) -> one tensor map; else cp.async
   p.use_tma = 0;
-  if (tc && d % 8 == 0 && cs / 64 <= kDMaxKc) {
+  p.nk = (d + 63) / 64;
+  // TIDE_DECODE_TMA=0: neither bulk nor TMA W loads (the cp.async path);
+  // TIDE_DECODE_PACKED=0: the tensor-map path over the stacked W (tests)
+  const char* tenv0 = getenv("TIDE_DECODE_TMA");
+  const char* penv = getenv("TIDE_DECODE_PACKED");
+  const bool no_tma = tenv0 && tenv0[0] == '0';
+  p.w_packed = (tc && d % 8 == 0 && !no_tma && !(penv && penv[0] == '0'))
+                   ? reinterpret_cast<const uint8_t*>(w_packed)
+                   : nullptr;
+  if (w_packed && (reinterpret_cast<uintptr_t>(w_packed) & 127))
+    return set_error(TIDE_ERR_ARG, "packed weights must be 128-byte aligned");
+  if (!p.w_packed && tc && d % 8 == 0 && cs / 64 <= kDMaxKc) {
     bool stacked = true;
     const char* w0 = reinterpret_cast<const char*>(w_ptrs[0]);
     for (int c = 1; c < C && stacked; ++c)
@@ -709,13 +1060,14 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
   // tensor-core path: slice CTAs of a checkpoint as one cluster (DSMEM
   // reduction) when S <= 16 and all C clusters fit; TIDE_DECODE_CLUSTER=0 disables
   const char* cenv = getenv("TIDE_DECODE_CLUSTER");  // read per call (tests switch it)
-  if (tc && !(cenv && cenv[0] == '0')) {
+  if (tc && C <= kAtomicMaxC && !(cenv && cenv[0] == '0')) {
     // widest slice first (S = 16, then 8): fewer bytes per CTA, if co-resident
     for (int cw = cs; cw <= 4 * cs; cw *= 2) {
       DecParams q = p;
       q.cs = cw;
       q.S = (d + cw - 1) / cw;
       if (q.S < 2 || q.S > 16 || q.cs % 64) continue;
+      if (q.w_packed && q.cs / 64 > kDMaxKc) q.w_packed = nullptr, q.use_tma = 0;
       const size_t smc = smem_tc(b, cw, NR) + smem_clu(b, q.S, NR);
       if (smc > 220 * 1024) break;
       int rc;
@@ -728,6 +1080,7 @@ extern "C" int tide_route_decode(const void* const* h_ptrs, int32_t C, int64_t l
       if (rc <= 0) return rc == 0 ? TIDE_OK : TIDE_ERR_CUDA;
     }
   }
+  if (p.w_packed && p.cs / 64 > kDMaxKc) p.w_packed = nullptr;  // cp.async fallback
   if (dtype == TIDE_BF16)
     return NR == 8 ? launch_kernel(decode_tc_kernel<true, 8, false>, p, smem, s, &attr[0])
                    : launch_kernel(decode_tc_kernel<true, 16, false>, p, smem, s, &attr[1]);

@@ -219,9 +219,19 @@ def _decode_plan(bank, ckpts, code, dev):
     stacked = torch.stack([w for w, _ in ws_w]).contiguous()
     step = stacked[0].numel() * stacked.element_size()
     base = stacked.data_ptr()
-    arrays = (N.ptr_array([base + i * step for i in range(len(routers))]),
-              N.ptr_array([u.data_ptr() for _, u in ws_w]), N.i64_array(ckpts))
-    return _decode_plans.put(key, owners, arrays + ((ws_w, stacked),))
+    w_arr = N.ptr_array([base + i * step for i in range(len(routers))])
+    # bf16 / f16: the routers' W in the decode kernel's shared-memory image,
+    # packed once (the kernel fetches its slices with 1-D bulk copies)
+    packed = None
+    if code != N.F32 and stacked.shape[2] % 8 == 0:
+        lib = N.load()
+        C, b, d = stacked.shape
+        packed = torch.empty(lib.tide_decode_packed_bytes(C, d, b), dtype=torch.uint8, device=dev)
+        N.check(lib.tide_decode_pack_weights(w_arr, C, d, b, code, packed.data_ptr(),
+                                             D.stream_handle(dev)), "tide_decode_pack_weights")
+    arrays = (w_arr, N.ptr_array([u.data_ptr() for _, u in ws_w]), N.i64_array(ckpts),
+              packed.data_ptr() if packed is not None else None)
+    return _decode_plans.put(key, owners, arrays + ((ws_w, stacked, packed),))
 
 
 def _decode_ok(n, d, code, b, ckpts, staged) -> bool:
@@ -373,15 +383,15 @@ def _bind_decode(staged, bank, config, ckpts, dev, s):
     n, d = final.shape
     code = D.dtype_code(final)
     plan = _decode_plan(bank, ckpts, code, dev)
-    w_arr, u_arr, l_arr = plan[:3]
+    w_arr, u_arr, l_arr, packed = plan[:4]
     b = _bottleneck(bank, ckpts)
     mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
     args = (N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
             w_arr, u_arr, b, l_arr, float(np.float32(bank.eps)),
             float(np.float32(config.exit_threshold)), int(config.k_min), mode, None, None,
-            0, None, D.workspace(dev, s).data_ptr(), s)
+            0, None, D.workspace(dev, s).data_ptr(), packed, s)
     # the plan (device weight copies the pointers refer to) lives with the entry
-    return (args, N.load().tide_route_decode, plan)
+    return (args, N.load().tide_route_decode_ex, plan)
 
 
 def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None):
@@ -398,13 +408,14 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
     code = D.dtype_code(final)
     b = _bottleneck(bank, ckpts)
     if _decode_ok(n, d, code, b, ckpts, staged):
-        w_arr, u_arr, l_arr = _decode_plan(bank, ckpts, code, dev)[:3]
+        plan = _decode_plan(bank, ckpts, code, dev)
+        w_arr, u_arr, l_arr, packed = plan[:4]
         mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
         out = torch.empty((n,), dtype=torch.int64, device=dev)  # the kernel writes every row
-        N.check(lib.tide_route_decode(
+        N.check(lib.tide_route_decode_ex(
             N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, d, code,
             w_arr, u_arr, b, l_arr, eps, theta, int(config.k_min), mode, None, None,
-            out.data_ptr(), None, ws, s), "tide_route_decode")
+            out.data_ptr(), None, ws, packed, s), "tide_route_decode")
         return out
     exit_layers = torch.full((n,), NO_EXIT, dtype=torch.int64, device=dev)
     if config.mode == BATCH_UNANIMOUS:
@@ -553,15 +564,16 @@ class DecodeStep:
                              "dtype (a converted copy would not see later writes)")
         self.out = out if out is not None else torch.empty((n,), dtype=torch.int64, device=dev)
         plan = _decode_plan(bank, ckpts, code, dev)
-        w_arr, u_arr, l_arr = plan[:3]
+        w_arr, u_arr, l_arr, packed = plan[:4]
         s = D.stream_handle(dev)
         mode = N.MODE_PER_TOKEN if config.mode == PER_TOKEN else N.MODE_BATCH_UNANIMOUS
         self._keep = (staged, plan, bank)
-        self._fn = N.load().tide_route_decode
+        self._fn = N.load().tide_route_decode_ex
         self._args = (N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n,
                       d, code, w_arr, u_arr, b, l_arr, float(np.float32(bank.eps)),
                       float(np.float32(config.exit_threshold)), int(config.k_min), mode, None,
-                      None, self.out.data_ptr(), None, D.workspace(dev, s).data_ptr(), s)
+                      None, self.out.data_ptr(), None, D.workspace(dev, s).data_ptr(), packed,
+                      s)
 
     def __call__(self) -> torch.Tensor:
         rc = self._fn(*self._args)

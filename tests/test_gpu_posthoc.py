@@ -262,6 +262,7 @@ def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch)
 
 
 @pytest.mark.parametrize("variant", [{"TIDE_DECODE_CLUSTER": "0"}, {"TIDE_DECODE_TMA": "0"},
+                                     {"TIDE_DECODE_PACKED": "0"}, {"TIDE_PDL": "0"},
                                      {"TIDE_DECODE_CLUSTER": "0", "TIDE_DECODE_TMA": "0"}])
 def test_decode_step_fallback_paths(variant, monkeypatch):
     """The global-ticket reduction and the cp.async W path give the same exit
@@ -400,3 +401,51 @@ def test_chain_cache_host_inputs_and_router_swap(monkeypatch):
     bank.routers[k0] = P.Router(layer=k0, w_down=r.w_down, w_up=r.w_up)
     for it in range(3):
         assert torch.equal(P.select_exits(states, bank, cfg), uncached(states, bank)), it
+
+
+@pytest.mark.parametrize("mode", [P.PER_TOKEN, P.BATCH_UNANIMOUS])
+@pytest.mark.parametrize("d,n", [(1024, 16), (512, 13), (2048, 3), (8192, 16)])
+def test_decode_step_cluster_row_owners(mode, d, n):
+    """Decode shapes whose cluster split leaves several rows per rank (small
+    d -> few slice-CTAs) or idle ranks (n < S), against the oracle; scores /
+    logits outputs and the exit count of the C ABI on the same launch."""
+    need_gpu()
+    from paper_2603_21365_b200 import _device as Dv
+    from paper_2603_21365_b200 import _native as N
+    from paper_2603_21365_b200 import runtime as R
+    ckpts, routers, states, bank, head = _big_case(36, d, n, "bf16", 77 + d + n, scale=0.3)
+    for theta in (0.5, 0.85):
+        cfg = P.RuntimeConfig(exit_threshold=theta, mode=mode)
+        exits = P.select_exits(states, bank, cfg).cpu().numpy()
+        scores, exc = {}, np.zeros(n, bool)
+        for k in ckpts:
+            s_, t, m = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
+            scores[k] = s_
+            exc |= np.abs(t - O.logit_of(theta)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
+        want = O.first_exit_from_scores(scores, theta, 0, mode)
+        if mode == P.BATCH_UNANIMOUS and exc.any():
+            exc[:] = True
+        assert np.all((exits == want) | exc), (theta, exits, want)
+    # the raw C entry with every output: scores / logits / exit count
+    code = N.BF16
+    plan = R._decode_plan(bank, list(ckpts), code, states[0].device)
+    C = len(ckpts)
+    sc = torch.empty(C * n, dtype=torch.float32, device="cuda")
+    lg = torch.empty(C * n, dtype=torch.float32, device="cuda")
+    ex = torch.empty(n, dtype=torch.int64, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    lib = N.load()
+    s = Dv.stream_handle()
+    N.check(lib.tide_route_decode_ex(
+        N.ptr_array([states[k + 1].data_ptr() for k in ckpts]), C, d, n, d, code, plan[0],
+        plan[1], 128, plan[2], 1e-6, 0.5, 0, N.MODE_PER_TOKEN if mode == P.PER_TOKEN else
+        N.MODE_BATCH_UNANIMOUS, sc.data_ptr(), lg.data_ptr(), ex.data_ptr(), cnt.data_ptr(),
+        Dv.workspace().data_ptr(), plan[3], s), "decode")
+    torch.cuda.synchronize()
+    sc, lg, ex = sc.cpu().numpy().reshape(C, n), lg.cpu().numpy().reshape(C, n), ex.cpu().numpy()
+    for i, k in enumerate(ckpts):
+        s_ref, t_ref, m_ref = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
+        assert O.logits_close(lg[i], t_ref, m_ref, RTOL["bf16"]).all()
+        np.testing.assert_array_equal(sc[i], np.array([O._sigma64(float(v)) for v in lg[i]],
+                                                      np.float32))
+    assert int(cnt[0]) == int((ex >= 0).sum())

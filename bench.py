@@ -9,6 +9,11 @@ resident batch (+ for N>1 the exit-map / compacted-index all-gathers over
 NCCL).  Inputs are 512 MiB per step, larger than the 126 MB L2, so no flush.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--extra]
+                    [--config headline|4|5] [--scaling weak|strong]
+
+`--config 5` / `--config 4` time the sharded legs of BASELINE configs 5 (exit
+selection over 20 checkpoints at d=8192, u8 exit-code all-gather) and 4
+(calibration labeller + count all-reduce), weak or strong scaling.
 
 `--impl reference` times the reference algorithm on the host cores instead
 (the oracle port of ee/router_ops.py:68-87 + ee/runtime.py:171 +
@@ -41,12 +46,14 @@ BYTES_PER_TOKEN = D * ELEM + 4 + 1 + 8
 WEIGHT_BYTES = B * D * ELEM + B * 4
 
 
-def workload_config(n_gpus: int) -> dict:
-    return {"workload": "fused RMSNorm+router+exit-mask+stable-compaction, 1 checkpoint, "
-                        "65,536 tokens/GPU, d=4096, b=128, bf16 rows+W_down, f32 w_up, "
-                        "theta=0.5, dense (no row index)",
-            "tokens_per_gpu": N_TOK, "d": D, "b": B, "theta": THETA,
-            "global_tokens": N_TOK * n_gpus, "parallelism": f"token-sharded x{n_gpus}",
+def workload_config(n_gpus: int, n_tok: int = N_TOK) -> dict:
+    return {"workload": f"fused RMSNorm+router+exit-mask+stable-compaction, 1 checkpoint, "
+                        f"{n_tok:,} tokens/GPU, d=4096, b=128, bf16 rows+W_down, f32 w_up, "
+                        f"theta=0.5, dense (no row index)"
+                        + ("; N>1: u8 exit-map all-gather + local global compaction"
+                           if n_gpus > 1 else ""),
+            "tokens_per_gpu": n_tok, "d": D, "b": B, "theta": THETA,
+            "global_tokens": n_tok * n_gpus, "parallelism": f"token-sharded x{n_gpus}",
             "l2": "inputs 512 MiB per step per GPU > 126 MB L2 (no flush needed)",
             "router_init": "N(0,1)*0.05, PCG64(202)", "rows": "N(0,1) bf16, torch cuda "
                                                              "Generator seeded 1234+rank"}
@@ -246,6 +253,7 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
 
     import paper_2603_21365_b200 as P
+    n_tok = N_TOK if args.scaling == "weak" else N_TOK // world
     from paper_2603_21365_b200 import _device as Dv
     from paper_2603_21365_b200 import _native as N
     from paper_2603_21365_b200 import sharding as S
@@ -256,18 +264,16 @@ def run_ours(args):
     router = P.Router(layer=3, w_down=orouter.w_down, w_up=orouter.w_up)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    h = torch.randn((N_TOK, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    h = torch.randn((n_tok, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
     wd, wu = P.router_ops.device_weights(router, N.BF16, dev)
-    gathered = S.ExitMapGather(N_TOK, world, dev) if world > 1 else None
-    scores = torch.empty(N_TOK, dtype=torch.float32, device=dev)
-    cont_idx = torch.empty(N_TOK, dtype=torch.int64, device=dev)
-    if gathered is not None:
-        # the kernel writes straight into the packed all-gather send buffer
-        mask, exit_idx, counts = gathered.exit_map, gathered.exit_idx, gathered.counts
-    else:
-        mask = torch.empty(N_TOK, dtype=torch.uint8, device=dev)
-        exit_idx = torch.empty(N_TOK, dtype=torch.int64, device=dev)
-        counts = torch.empty(2, dtype=torch.int64, device=dev)
+    gathered = S.ExitMapGather(n_tok, world, dev) if world > 1 else None
+    scores = torch.empty(n_tok, dtype=torch.float32, device=dev)
+    cont_idx = torch.empty(n_tok, dtype=torch.int64, device=dev)
+    exit_idx = torch.empty(n_tok, dtype=torch.int64, device=dev)
+    counts = torch.empty(2, dtype=torch.int64, device=dev)
+    # N > 1: the kernel writes its u8 mask straight into the all-gather send buffer
+    mask = gathered.exit_map if gathered is not None else torch.empty(n_tok, dtype=torch.uint8,
+                                                                      device=dev)
     lib = N.load()
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
@@ -281,17 +287,18 @@ def run_ours(args):
     def step(kernel_events=None, collective=True, flags=N.ROUTE_INPUTS_READY):
         if kernel_events is not None:
             kernel_events[0].record(stream)
-        rc = lib.tide_route_ex(h.data_ptr(), D, N_TOK, None, N_TOK, D, N.BF16, None,
+        rc = lib.tide_route_ex(h.data_ptr(), D, n_tok, None, n_tok, D, N.BF16, None,
                                wd.data_ptr(), wu.data_ptr(), B, EPS, THETA, 3, scores.data_ptr(),
                                None, mask.data_ptr(), exit_idx.data_ptr(), cont_idx.data_ptr(), 0,
                                None, counts.data_ptr(), ws, flags, sh)
-        launches["n"] += 1
+        launches["n"] += 1 + (gathered is not None and collective)
         if kernel_events is not None:
             kernel_events[1].record(stream)
         if rc:
             N.check(rc, "tide_route")
         if gathered is not None and collective:
-            gathered.all_gather()  # C1 + C2 in one collective
+            gathered.all_gather()                        # C1: 1 byte per token
+            gathered.global_exit_indices(sync=False)     # C2: one local scan
 
     def barrier():
         if world > 1:
@@ -378,24 +385,25 @@ def run_ours(args):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     ms_per_step = ms_max / args.steps
-    value = N_TOK * world * args.steps / (ms_max / 1e3)
+    value = n_tok * world * args.steps / (ms_max / 1e3)
 
     # e2e through the public API with HOST buffers (pinned), copies in the timed region
     h_host = h.cpu().pin_memory()
-    mask_host = torch.empty(N_TOK, dtype=torch.uint8).pin_memory()
-    idx_host = torch.empty(N_TOK, dtype=torch.int64).pin_memory()
+    mask_host = torch.empty(n_tok, dtype=torch.uint8).pin_memory()
+    idx_host = torch.empty(n_tok, dtype=torch.int64).pin_memory()
     cnt_host = torch.empty(2, dtype=torch.int64).pin_memory()
     h_dev = torch.empty_like(h)
 
     def e2e_fused_step():
         h_dev.copy_(h_host, non_blocking=True)
-        rc = lib.tide_route(h_dev.data_ptr(), D, N_TOK, None, N_TOK, D, N.BF16, None,
+        rc = lib.tide_route(h_dev.data_ptr(), D, n_tok, None, n_tok, D, N.BF16, None,
                             wd.data_ptr(), wu.data_ptr(), B, EPS, THETA, 3, scores.data_ptr(),
                             None, mask.data_ptr(), exit_idx.data_ptr(), cont_idx.data_ptr(), 0,
                             None, counts.data_ptr(), ws, sh)
         N.check(rc, "tide_route")
         if gathered is not None:
             gathered.all_gather()  # the same step as the device-resident one
+            gathered.global_exit_indices(sync=False)
         mask_host.copy_(mask, non_blocking=True)
         idx_host.copy_(exit_idx, non_blocking=True)
         cnt_host.copy_(counts, non_blocking=True)
@@ -415,20 +423,20 @@ def run_ours(args):
     e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = N_TOK * world * e2e_steps / (float(e_ms.item()) / 1e3)
+    e2e_value = n_tok * world * e2e_steps / (float(e_ms.item()) / 1e3)
 
     if rank == 0:
         peaks = measured_peaks()
         # average launch duration over the timed region: at N=1 the step is exactly one
         # launch, back to back, so region time / launches; at N>1 the per-launch events
         kavg = (ms_total / gpu_launches) if world == 1 else sum(kernel_ms) / len(kernel_ms)
-        alg_bytes = N_TOK * BYTES_PER_TOKEN + WEIGHT_BYTES
+        alg_bytes = n_tok * BYTES_PER_TOKEN + WEIGHT_BYTES
         achieved = alg_bytes / (kavg / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic", "config": workload_config(world),
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic", "config": workload_config(world, n_tok),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                          "traffic": ncu_traffic("route_tc_kernel"),
@@ -436,16 +444,16 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "frac_of_8TBs_spec": achieved / 8000.0},
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": N_TOK * D * ELEM,
-                    "d2h_bytes_per_step": N_TOK * 1 + N_TOK * 8 + 16},
+                    "h2d_bytes_per_step": n_tok * D * ELEM,
+                    "d2h_bytes_per_step": n_tok * 1 + n_tok * 8 + 16},
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "clocks_sustained": dict(clk_sustained, window="0.6 s of the same step back to back, "
                                                           "after the timed region",
                                      ms_per_launch=sustained_ms,
-                                     value_per_gpu=N_TOK / (sustained_ms / 1e3)),
+                                     value_per_gpu=n_tok / (sustained_ms / 1e3)),
             "extra": {"tensor_cores": bool(lib.tide_route_uses_tensor_cores(N.BF16, D, B)),
-                      "tflops_tensor": 2.0 * D * B * N_TOK / (kavg / 1e3) / 1e12,
+                      "tflops_tensor": 2.0 * D * B * n_tok / (kavg / 1e3) / 1e12,
                       "kernel_ms_min": min(kernel_ms), "kernel_ms_max": max(kernel_ms),
                       "kernel_ms_inputs_wait": ms_wait},
         }
@@ -463,6 +471,189 @@ def run_ours(args):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# sharded legs of BASELINE configs 4 and 5 (bench.py --config 4|5)
+# ---------------------------------------------------------------------------
+def _dist_init():
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    one_gpu = os.environ.get("TIDE_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    return rank, world, local, dev
+
+
+def _timed_steps(step, args, dev, world, local):
+    """W warm-up steps, then K steps between barriers + syncs, CUDA events on
+    the current stream; returns (max-over-ranks ms, clocks)."""
+    import torch
+    import torch.distributed as dist
+    clocks = ClockSampler(local, period_ms=20)
+    clocks.start()
+    for _ in range(args.warmup):
+        step()
+    stream = torch.cuda.current_stream(dev)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    w0 = time.time()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.mark(w0, time.time())
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return float(ms.item()), clocks.stop()
+
+
+def run_config5(args):
+    """BASELINE config 5: 70B shape (d=8192, 80 layers, 20 checkpoint routers),
+    65,536-token prefill batch token-sharded over the GPUs (strong: 65,536/N
+    tokens per GPU; weak: 8,192 per GPU).  Step = the per-token exit
+    selection on the local shard (peeling chain, sharding.select_exits_shard)
+    + the u8 exit-code all-gather (C1) + the local global compaction (C2)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local, dev = _dist_init()
+    import paper_2603_21365_b200 as P
+    from paper_2603_21365_b200 import sharding as S
+    from oracle import tide_oracle as O
+
+    L, d, b, theta = 80, 8192, 128, args.theta if args.theta is not None else 0.7
+    n_local = 65536 // world if args.scaling == "strong" else 8192
+    g = np.random.Generator(np.random.PCG64(5))
+    ckpts = O.checkpoint_layers(L, 4)
+    routers = {k: O.make_router(d, b, k, g, scale=0.06) for k in ckpts}
+    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5000 + rank)
+    states = [None] * (L + 1)
+    for k in list(ckpts) + [L - 1]:
+        t = torch.empty((n_local, d), dtype=torch.bfloat16, device=dev)
+        for r0 in range(0, n_local, 8192):
+            r1 = min(n_local, r0 + 8192)
+            t[r0:r1] = torch.randn((r1 - r0, d), generator=gen, device=dev).to(torch.bfloat16)
+        states[k + 1] = t
+    for i in range(L + 1):
+        if states[i] is None:
+            states[i] = states[L]
+    cfg = P.RuntimeConfig(exit_threshold=theta)
+    gat = S.ExitMapGather(n_local, world, dev)
+
+    def step():
+        S.select_exits_shard(states, bank, cfg, gat)
+        gat.global_exit_indices(sync=False)
+
+    ms, clk = _timed_steps(step, args, dev, world, local)
+    layers = gat.global_exit_layers().cpu().numpy()
+    exit_rate = float((layers >= 0).mean())
+    loc = layers[rank * n_local:(rank + 1) * n_local]
+    remaining, peeled = n_local, 0
+    for k in ckpts:
+        peeled += remaining * (d * 2 + 21)
+        remaining -= int((loc == k).sum())
+    ms_step = ms / args.steps
+    if rank == 0:
+        line = {"metric": "exit-selected tokens/sec, config 5 (70B shape, 20 checkpoints, "
+                          "d=8192, bf16), token-sharded", "value": n_local * world / (ms_step / 1e3),
+                "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": "config 5: per-token peeling exit selection over 20 "
+                                       "checkpoint routers + u8 exit-code all-gather + global "
+                                       "compaction", "tokens_per_gpu": n_local,
+                           "global_tokens": n_local * world, "d": d, "b": b, "theta": theta,
+                           "layers": L, "checkpoints": len(ckpts),
+                           "parallelism": f"token-sharded x{world}",
+                           "l2": "captures 21 x n x 16 KiB per GPU, read once per step"},
+                "exit_rate": exit_rate,
+                "roofline": {"bound": "hbm", "achieved": peeled / (ms_step / 1e3) / 1e9,
+                             "peak": measured_peaks()["hbm_gbs"], "unit": "GB/s",
+                             "frac": peeled / (ms_step / 1e3) / 1e9 / measured_peaks()["hbm_gbs"],
+                             "traffic": None, "algorithmic_bytes_per_step_rank0": peeled,
+                             "bytes_rule": "sum over checkpoints of live rows x (d*2 + 21)"},
+                "collective_bytes_per_rank": n_local, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_config4(args):
+    """BASELINE config 4: calibration labelling, cosine similarity of 8
+    checkpoints vs the final layer over 2,000 x 512 = 1,024,000 tokens at
+    d=4096 bf16, token-sharded (strong: 1,024,000 / N per GPU; weak:
+    1,024,000 per GPU).  Step = sharding.label_shard: one labeller launch over
+    the local shard + the all-reduce of zero-norm / positive counts."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local, dev = _dist_init()
+    import paper_2603_21365_b200  # noqa: F401
+    from paper_2603_21365_b200 import sharding as S
+
+    n_all, d, C, tau = 1_024_000, 4096, 8, 0.98
+    n_local = n_all // world if args.scaling == "strong" else n_all
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4000 + rank)
+    fin = torch.empty((n_local, d), dtype=torch.bfloat16, device=dev)
+    cks = {3 + 4 * i: torch.empty_like(fin) for i in range(C)}
+    for r0 in range(0, n_local, 131072):
+        r1 = min(n_local, r0 + 131072)
+        f = torch.randn((r1 - r0, d), generator=gen, device=dev)
+        fin[r0:r1] = f.to(torch.bfloat16)
+        for i, t in enumerate(cks.values()):  # checkpoints drift toward the final layer
+            noise = 0.1 + 0.5 * (C - 1 - i) / C
+            t[r0:r1] = (f + noise * torch.randn((r1 - r0, d), generator=gen,
+                                                device=dev)).to(torch.bfloat16)
+    out = {}
+
+    def step():
+        out.update(S.label_shard(cks, fin, tau, world))
+
+    ms, clk = _timed_steps(step, args, dev, world, local)
+    ms_step = ms / args.steps
+    byts = n_local * (C + 1) * d * 2 + n_local * C * 5
+    if rank == 0:
+        gbs = byts / (ms_step / 1e3) / 1e9
+        line = {"metric": "labelled tokens/sec, config 4 (cosine labeller, 8 checkpoints + final, "
+                          "d=4096 bf16), token-sharded", "value": n_local * world / (ms_step / 1e3),
+                "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": "config 4: one-pass cosine labeller + count all-reduce",
+                           "tokens_per_gpu": n_local, "global_tokens": n_local * world, "d": d,
+                           "checkpoints": C, "tau": tau, "parallelism": f"token-sharded x{world}",
+                           "l2": f"{byts / 2**30:.1f} GiB read per step per GPU > 126 MB L2"},
+                "positives_rank0": [int(x) for x in out["positives"].cpu()],
+                "roofline": {"bound": "hbm", "achieved": gbs, "peak": measured_peaks()["hbm_gbs"],
+                             "unit": "GB/s", "frac": gbs / measured_peaks()["hbm_gbs"],
+                             "traffic": None, "algorithmic_bytes_per_step": byts},
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -472,11 +663,23 @@ def main():
     ap.add_argument("--extra", action="store_true", help="also time configs 2-5 (slower)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--config", default="headline", choices=["headline", "4", "5"],
+                    help="headline (BASELINE metric), or the sharded config-4 / config-5 legs")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="weak: fixed tokens per GPU (headline / config 5 default); strong: "
+                         "fixed global tokens (config 4 default)")
+    ap.add_argument("--theta", type=float, default=None, help="config 5 exit threshold")
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = "strong" if args.config == "4" else "weak"
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "5":
+        return run_config5(args)
+    if args.config == "4":
+        return run_config4(args)
     return run_ours(args)
 
 

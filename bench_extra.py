@@ -121,9 +121,9 @@ def config4(n=1_024_000, d=4096, C=8):
     return out
 
 
-def config5():
+def config5(theta=0.7):
     ckpts, states, bank = _case(80, 8192, 8192, torch.bfloat16, 5, 0.06)
-    cfg = P.RuntimeConfig(exit_threshold=0.7)
+    cfg = P.RuntimeConfig(exit_threshold=theta)
     exits = P.select_exits(states, bank, cfg)
     ms = _time(lambda: P.select_exits(states, bank, cfg))
     gms = _graph_time(lambda: P.select_exits(states, bank, cfg))
@@ -132,7 +132,8 @@ def config5():
     for k in ckpts:
         peeled += remaining * (8192 * 2 + 21)
         remaining -= int((e == k).sum())
-    return {"config": "5: 70B prefill shard, L=80 (20 ckpts), d=8192, 8,192 tok/GPU, bf16",
+    return {"config": f"5: 70B prefill shard, L=80 (20 ckpts), d=8192, 8,192 tok/GPU, bf16, "
+                      f"per-token theta={theta}",
             "ms_api": ms, "ms_graph": gms, "tokens_per_s": 8192 / (gms / 1e3),
             "peeled_bytes": peeled, "gbs_graph": peeled / (gms / 1e3) / 1e9,
             "exit_rate": float((e >= 0).mean()), "launches": len(ckpts)}
@@ -172,6 +173,13 @@ def training(n=65_536, d=4096, epochs=2):
             "rows_per_s": n * epochs / sec, "accuracy": st.accuracy}
 
 
+def chain_sweep():
+    """Peeling-chain configs 2 and 5 across thresholds, down to the worst case
+    theta = 1.0 where no row ever exits and every link routes every row."""
+    return ([config2(t) for t in (0.5, 0.7, 0.85, 1.0)]
+            + [config5(t) for t in (0.7, 0.85, 1.0)])
+
+
 def run_extra(dev=None):
     out = []
     for fn in (config1, config2, config3,
@@ -186,5 +194,10 @@ def run_extra(dev=None):
 
 if __name__ == "__main__":
     import json
-    for r in run_extra():
-        print(json.dumps(r))
+    import sys
+    if len(sys.argv) > 1 and sys.argv[1] == "sweep":
+        for r in chain_sweep():
+            print(json.dumps(r), flush=True)
+    else:
+        for r in run_extra():
+            print(json.dumps(r), flush=True)

@@ -122,6 +122,16 @@ int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int
                  void* cont_rows, int64_t* counts, void* workspace, void* stream);
 
 /*
+ * u8 exit codes for the multi-GPU exit-map exchange (the
+ * reference's exit map is ee/runtime.py:153-178's int64 exit_layers):
+ * code[i] = exit_layers[i] + 1, so NO_EXIT (-1) -> 0 and checkpoint k -> k+1
+ * (layers must lie in [-1, 254]).  tide_exit_decode is the inverse.  A
+ * gathered code array is itself a valid tide_compact mask (nonzero = exited).
+ */
+int tide_exit_encode(const int64_t* exit_layers, int64_t n, uint8_t* code, void* stream);
+int tide_exit_decode(const uint8_t* code, int64_t n, int64_t* exit_layers, void* stream);
+
+/*
  * exit_scatter (ee/router_ops.py:170-176, normalize = 0) and exit_projection
  * (ee/router_ops.py:179-188, normalize = 1):
  *   out[positions[j]] = normalize ? rmsnorm(rows[src(j)], gain, eps) : rows[src(j)]

@@ -253,4 +253,17 @@ int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
+int tide_exit_encode(const int64_t* exit_layers, int64_t n, uint8_t* code, void* stream) {
+  if (n < 0 || (n > 0 && (!exit_layers || !code)))
+    return set_error(TIDE_ERR_ARG, "tide_exit_encode: bad arguments");
+  return exit_code_launch(exit_layers, n, code, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tide_exit_decode(const uint8_t* code, int64_t n, int64_t* exit_layers, void* stream) {
+  if (n < 0 || (n > 0 && (!exit_layers || !code)))
+    return set_error(TIDE_ERR_ARG, "tide_exit_decode: bad arguments");
+  return exit_code_launch(exit_layers, n, const_cast<uint8_t*>(code), 1,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

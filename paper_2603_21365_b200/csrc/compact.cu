@@ -170,4 +170,37 @@ int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const i
   return check_launch("compact_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// u8 exit codes for the multi-GPU exchange: code = layer + 1
+// for a token that exited at checkpoint `layer`, 0 for NO_EXIT (-1).  One byte
+// per token is what crosses NVLink; every rank then rebuilds the global exit
+// list with one compact_kernel scan of the gathered codes (nonzero = exited).
+__global__ void exit_encode_kernel(const int64_t* __restrict__ layers, int64_t n,
+                                   uint8_t* __restrict__ code) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    code[i] = (uint8_t)(layers[i] + 1);
+}
+
+__global__ void exit_decode_kernel(const uint8_t* __restrict__ code, int64_t n,
+                                   int64_t* __restrict__ layers) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    layers[i] = (int64_t)code[i] - 1;
+}
+
+int exit_code_launch(const int64_t* layers, int64_t n, uint8_t* code, int decode,
+                     cudaStream_t stream) {
+  if (n == 0) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256,
+                                                               (int64_t)sm_count(dev) * 8));
+  if (decode)
+    exit_decode_kernel<<<grid, 256, 0, stream>>>(code, n, const_cast<int64_t*>(layers));
+  else
+    exit_encode_kernel<<<grid, 256, 0, stream>>>(layers, n, code);
+  return check_launch(decode ? "exit_decode_kernel" : "exit_encode_kernel");
+}
+
 }  // namespace tide

@@ -66,5 +66,7 @@ int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const i
                    int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
                    int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,
                    void* cont_rows, int64_t* counts, void* workspace, cudaStream_t stream);
+int exit_code_launch(const int64_t* layers, int64_t n, uint8_t* code, int decode,
+                     cudaStream_t stream);
 
 }  // namespace tide

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2, gloo, CPU) test of the token-sharding host
 logic: contiguous shards, C1 exit-map all-gather, C2 compacted-index
 assembly.  The per-rank compute is the oracle here (no GPU); on B200 the
-same host code wraps the kernels with NCCL.  The gathered result must be
+same host code wraps the kernels with NCCL (tests/test_gpu_sharding.py runs
+the real kernels through it on two ranks).  The gathered result must be
 bit-identical to the single-process partition."""
 
 import os
@@ -22,6 +23,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _oracle_compactor(mask, out_idx, counts):
+    """The CPU tests' stand-in for tide_compact (the oracle's stable partition)."""
+    from oracle import tide_oracle as O
+    e, c = O.compact_indices(mask.numpy())
+    out_idx[: len(e)] = torch.from_numpy(e)
+    counts.copy_(torch.tensor([len(e), len(c)], dtype=torch.int64))
+
+
 def _worker(rank, world, port, n, seed, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -37,14 +46,19 @@ def _worker(rank, world, port, n, seed, q):
         e, c = idx[local_mask], idx[~local_mask]
         n_local = s1 - s0
         if n % world == 0:
-            gat = S.ExitMapGather(n_local, world, "cpu")
-            # what tide_route writes into the packed send buffer's views
-            gat.exit_idx[: len(e)] = torch.from_numpy(e)
+            gat = S.ExitMapGather(n_local, world, "cpu", compactor=_oracle_compactor)
+            # what tide_route writes into the send buffer: the shard's u8 mask
             gat.exit_map.copy_(torch.from_numpy(local_mask.astype(np.uint8)))
-            gat.counts.copy_(torch.tensor([len(e), len(c)], dtype=torch.int64))
             gat.all_gather()
-            glob_exit = gat.global_exit_indices().numpy()
+            glob_exit = gat.global_exit_indices().numpy().copy()
             glob_map = gat.global_exit_map().numpy().astype(bool)
+            # exit codes of a multi-checkpoint map: encode -> gather -> decode
+            gat.encode(torch.from_numpy(layer_all[s0:s1]))
+            gat.all_gather()
+            glob_codes = gat.global_exit_layers().numpy()
+            glob_code_exit = gat.global_exit_indices().numpy().copy()
+            assert np.array_equal(glob_codes, layer_all)
+            assert np.array_equal(glob_code_exit, glob_exit)
         else:
             glob_exit = None
             glob_map = None

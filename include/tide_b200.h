@@ -267,6 +267,22 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
  * the remaining links there), tide_capture_cond_close ends that body.  Outside
  * capture, cond_create returns handle 0 and the links run as plain launches.
  */
+/*
+ * tide_route_tail with a lower bound: the tail handles the live rows only when
+ * n_min <= *n_dev <= n_limit (else it leaves *tail_count = *n_dev for the
+ * links).  n_limit >= cap makes it a WIDE tail: one cluster per live tile and
+ * checkpoint, any live count — the speculative "score every remaining
+ * checkpoint" step the chain takes right after its first link when few rows
+ * exited there (n_min = the caller's break-even live count).
+ * tide_route_tail(...) == tide_route_tail_ex(..., n_min = 0, ...).
+ */
+int tide_route_tail_ex(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t rows_total,
+                       int32_t d, int32_t dtype, const int64_t* row_idx, const int64_t* n_dev,
+                       int64_t cap, int64_t n_min, int64_t n_limit, const void* const* w_ptrs,
+                       const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
+                       float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
+                       uint64_t cond_handle, void* workspace, void* stream);
+
 int tide_capture_cond_create(void* stream, uint64_t* handle);
 int tide_capture_cond_open(void* stream, uint64_t handle, void** body_stream);
 int tide_capture_cond_close(void* body_stream);

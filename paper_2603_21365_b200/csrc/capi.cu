@@ -144,6 +144,18 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
                     const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
                     float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
                     uint64_t cond_handle, void* workspace, void* stream) {
+  return tide_route_tail_ex(h_ptrs, C, ld_h, rows_total, d, dtype, row_idx, n_dev, cap, 0, n_limit,
+                            w_ptrs, wup_ptrs, b, layers, eps, theta, scores, exit_layers,
+                            tail_count, cond_handle, workspace, stream);
+}
+
+int tide_route_tail_ex(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t rows_total,
+                       int32_t d, int32_t dtype, const int64_t* row_idx, const int64_t* n_dev,
+                       int64_t cap, int64_t n_min, int64_t n_limit, const void* const* w_ptrs,
+                       const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
+                       float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
+                       uint64_t cond_handle, void* workspace, void* stream) {
+  if (n_min < 0) return set_error(TIDE_ERR_ARG, "tide_route_tail: n_min < 0");
   if (C < 1 || !h_ptrs || !w_ptrs || !wup_ptrs || !layers)
     return set_error(TIDE_ERR_ARG, "tide_route_tail: bad checkpoint arrays");
   if (d < 1 || b < 1 || cap < 1 || ld_h < d || rows_total < 1 || n_limit < 0)
@@ -175,6 +187,7 @@ int tide_route_tail(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t 
   a.scores = scores;
   a.exit_layers = exit_layers;
   a.workspace = workspace;
+  a.n_min = n_min;
   if (dtype == TIDE_F32)  // CUDA-core kernel, f32 products (the 1e-5 contract)
     return route_simt_tail_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, layers, n_limit, tail_count,
                                   (unsigned long long)cond_handle,

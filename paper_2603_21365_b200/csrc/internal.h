@@ -34,6 +34,7 @@ struct RouteArgs {
   int64_t* counts;
   void* workspace;
   uint32_t flags;  // TIDE_ROUTE_* (tide_route_ex)
+  int64_t n_min;   // chain tail: handle the live rows only when n_min <= n <= n_limit
 };
 
 int set_error(int code, const char* fmt, ...);
@@ -57,7 +58,7 @@ int route_simt_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                            const int64_t* layers, int64_t n_limit, int64_t* tail_count,
                            unsigned long long cond, cudaStream_t stream);
 int chain_resolve_launch(const float* scores, int64_t cap, int C, const int64_t* layers,
-                         float theta, const int64_t* n_dev, int64_t n_limit,
+                         float theta, const int64_t* n_dev, int64_t n_min, int64_t n_limit,
                          const int64_t* row_idx, int64_t* exit_layers, int64_t* tail_count,
                          unsigned long long cond, cudaStream_t stream);
 bool route_tf32_supported(int d, int b);

@@ -500,7 +500,7 @@ struct SimtTailParams {
   const void* hs[kSimtTailC];
   const void* ws[kSimtTailC];
   const float* wups[kSimtTailC];
-  int64_t cap, n_limit;
+  int64_t cap, n_limit, n_min;
 };
 
 template <typename XT>
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kSThreads) route_simt_tail_kernel(const __grid
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int c = blockIdx.y;
   const int64_t n = *p.n_dev;
-  if (n > tp.n_limit) return;
+  if (n > tp.n_limit || n < tp.n_min) return;
   const XT* h = reinterpret_cast<const XT*>(tp.hs[c]);
   const XT* W = reinterpret_cast<const XT*>(tp.ws[c]);
   const float* w_up = tp.wups[c];
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(kSThreads, 1) route_simt_tail_wide_kernel(cons
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int c = blockIdx.y;
   const int64_t n = *p.n_dev;
-  if (n > tp.n_limit) return;
+  if (n > tp.n_limit || n < tp.n_min) return;
   const XT* h = reinterpret_cast<const XT*>(tp.hs[c]);
   const XT* W = reinterpret_cast<const XT*>(tp.ws[c]);
   const float* w_up = tp.wups[c];
@@ -625,6 +625,7 @@ int route_simt_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
   }
   tp.cap = a.n;
   tp.n_limit = std::min<int64_t>(n_limit, a.n);
+  tp.n_min = a.n_min;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(route_simt_tail_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVSmem);
@@ -645,7 +646,7 @@ int route_simt_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
   }
   if (rc) return rc;
   return chain_resolve_launch((const float*)a.scores, a.n, C, layers, a.theta, a.n_dev,
-                              tp.n_limit, a.row_idx, a.exit_layers, tail_count, cond, stream);
+                              tp.n_min, tp.n_limit, a.row_idx, a.exit_layers, tail_count, cond, stream);
 }
 
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream) {

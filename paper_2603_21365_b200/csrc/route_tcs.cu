@@ -51,12 +51,13 @@ struct WMaps {  // W_down tensor map per checkpoint (NC = 1: the plain route)
 };
 
 struct SplitParams {
-  // chain tail (NC > 1): checkpoint c = blockIdx.y reads its rows from
+  // chain tail (NC > 1): checkpoint c (see the grid order in the kernel) reads its rows from
   // h_bases[c] and w_ups[c] and writes scores[c * cap + position]; the launch
   // does nothing when the live count exceeds n_limit
   const uint8_t* h_bases[kMaxTailC];
   const float* w_ups[kMaxTailC];
-  int64_t cap, n_limit;
+  int64_t cap, n_limit, n_min;
+  int32_t nc;  // checkpoints of a tail launch (NC > 1)
   int64_t n_host;
   const int64_t* n_dev;
   int64_t rows_total;
@@ -135,7 +136,14 @@ template <bool kBF16, int NC>
 __global__ void __launch_bounds__(kThreadsS, 1)
     route_tcs_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ WMaps<NC> wm,
                      const __grid_constant__ SplitParams p) {
-  const int ck = NC > 1 ? (int)blockIdx.y : 0;
+  // Chain tail (NC > 1): the grid is [X clusters per checkpoint] x C along x,
+  // checkpoint fastest — cluster g serves checkpoint g % C and per-checkpoint
+  // cluster g / C, so the clusters of the low (live) tiles of EVERY checkpoint
+  // come first in launch order and the idle rest of a wide tail drains after.
+  const uint32_t cl_lin = blockIdx.x / (uint32_t)p.ks;
+  const int ck = NC > 1 ? (int)(cl_lin % (uint32_t)p.nc) : 0;
+  const uint32_t cl_idx = NC > 1 ? cl_lin / (uint32_t)p.nc : cl_lin;     // cluster within its checkpoint
+  const uint32_t cl_cnt = NC > 1 ? gridDim.x / (uint32_t)p.nc : gridDim.x;  // CTAs per checkpoint
   const CUtensorMap& tm_w = wm.m[ck];
   const uint8_t* const h_base = NC > 1 ? p.h_bases[ck] : p.h_base;
   const float* const w_up_c = NC > 1 ? p.w_ups[ck] : p.w_up;
@@ -168,6 +176,20 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   // before griddepcontrol.wait, so it overlaps the previous link's tail; the
   // live count and row index it wrote are read after.
   if (threadIdx.x == 0) griddep_launch_dependents();
+  if (NC > 1) {
+    // tail: a cluster with no live tile leaves before any setup (it only counts
+    // itself done for the workspace epoch)
+    griddep_wait();
+    const int64_t n0 = p.n_dev ? *p.n_dev : p.n_host;
+    const int64_t nt0 = (n0 > p.n_limit || n0 < p.n_min) ? 0 : (n0 + 127) / 128;
+    int ks0 = p.ks;
+    while (ks0 > 1 && nt0 * ks0 > (int64_t)cl_cnt) ks0 >>= 1;
+    if ((int64_t)cl_idx * (p.ks / ks0) >= nt0) {
+      __syncthreads();
+      if (threadIdx.x == 0) launch_done(p.ws);
+      return;
+    }
+  }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_w);
     if (p.row_idx == nullptr) prefetch_tmap(&tm_h);
@@ -187,11 +209,12 @@ __global__ void __launch_bounds__(kThreadsS, 1)
   griddep_wait();
   const uint32_t crank = cluster_rank();
   const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
-  const int64_t ntiles = (NC > 1 && n > p.n_limit) ? 0 : (n + 127) / 128;  // tail: over the limit -> idle
+  // tail: outside [n_min, n_limit] -> idle
+  const int64_t ntiles = (NC > 1 && (n > p.n_limit || n < p.n_min)) ? 0 : (n + 127) / 128;
   int ks = p.ks;
-  while (ks > 1 && ntiles * ks > (int64_t)gridDim.x) ks >>= 1;
+  while (ks > 1 && ntiles * ks > (int64_t)cl_cnt) ks >>= 1;
   const uint32_t rank = crank % (uint32_t)ks, gbase = crank - rank;
-  const int64_t tile = (int64_t)(blockIdx.x / p.ks) * (p.ks / ks) + crank / (uint32_t)ks;
+  const int64_t tile = (int64_t)cl_idx * (p.ks / ks) + crank / (uint32_t)ks;
   const int cw = p.bp / ks;
   const uint32_t tag = launch_tag(p.ws);
   if (tile >= ntiles) {
@@ -200,7 +223,10 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       p.counts[0] = 0;
       p.counts[1] = 0;
     }
-    if (ntiles > 0) {  // some group of the cluster may be live: keep its barrier count
+    // another group of this cluster is live: keep its barrier count (a wholly
+    // idle cluster — most of a wide chain tail's grid when few rows are
+    // left — leaves at once)
+    if ((int64_t)cl_idx * (p.ks / ks) < ntiles) {
       cluster_arrive_relaxed();
       cluster_wait();
       cluster_arrive_relaxed();
@@ -737,11 +763,12 @@ int tcs_launch(const RouteArgs& a, const SplitParams& p, const WMaps<NC>& wm, ui
 // rule of ee/runtime.py:166-178 over the tail's checkpoints, in order) and the
 // live count the following links read (0 when the tail handled the rows).
 __global__ void chain_resolve_kernel(const float* scores, int64_t cap, int nc, TailLayers layers,
-                                     float theta, const int64_t* n_dev, int64_t n_limit,
+                                     float theta, const int64_t* n_dev, int64_t n_min,
+                                     int64_t n_limit,
                                      const int64_t* row_idx, int64_t* exit_layers,
                                      int64_t* tail_count, unsigned long long cond) {
   const int64_t n = *n_dev;
-  const bool handled = n <= n_limit;
+  const bool handled = n >= n_min && n <= n_limit;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *tail_count = handled ? 0 : n;
     // in a captured CUDA graph: the IF node holding the remaining links runs
@@ -809,14 +836,23 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
       ks = c;
       break;
     }
-  const int grid = std::max(ks, per / ks * ks);
-  n_limit = std::min<int64_t>(n_limit, (int64_t)grid * 128);
+  int grid = std::max(ks, per / ks * ks);
+  if (n_limit >= a.n) {
+    // wide tail (n_limit >= capacity): every live count is handled; one
+    // cluster per live tile and checkpoint, in as many waves as it takes
+    // (clusters past the live tiles exit at once)
+    grid = std::max<int64_t>(grid, (a.n + 127) / 128 * ks);
+    n_limit = a.n;
+  } else {
+    n_limit = std::min<int64_t>(n_limit, (int64_t)grid * 128);
+  }
   SplitParams p{};
   TcsLayout L;
   int rc;
   if ((rc = tcs_params(a, ks, p, L))) return rc;
   p.cap = a.n;
   p.n_limit = n_limit;
+  p.n_min = a.n_min;
   p.logits = nullptr;  // scores only; no mask / compaction / exit layers in the routing step
   p.mask = nullptr;
   p.exit_idx = nullptr;
@@ -831,14 +867,17 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
     p.w_ups[c] = wup_ptrs[c];
     if ((rc = make_map(&wm.m[c], w_ptrs[c], a.dtype, a.d, a.b, a.d, 64, L.npad))) return rc;
   }
-  if ((rc = tcs_launch<kMaxTailC>(a, p, wm, L.smem_bytes, ks, grid, C, stream, "route_tcs_kernel (tail)")))
+  p.nc = C;
+  if ((rc = tcs_launch<kMaxTailC>(a, p, wm, L.smem_bytes, ks, grid * C, 1, stream,
+                                  "route_tcs_kernel (tail)")))
     return rc;
-  return chain_resolve_launch((const float*)a.scores, a.n, C, layers, a.theta, a.n_dev, n_limit,
+  return chain_resolve_launch((const float*)a.scores, a.n, C, layers, a.theta, a.n_dev, a.n_min,
+                              n_limit,
                               a.row_idx, a.exit_layers, tail_count, cond, stream);
 }
 
 int chain_resolve_launch(const float* scores, int64_t cap, int C, const int64_t* layers,
-                         float theta, const int64_t* n_dev, int64_t n_limit,
+                         float theta, const int64_t* n_dev, int64_t n_min, int64_t n_limit,
                          const int64_t* row_idx, int64_t* exit_layers, int64_t* tail_count,
                          unsigned long long cond, cudaStream_t stream) {
   if (C < 1 || C > kMaxTailC) return set_error(TIDE_ERR_ARG, "resolve: C must be in [1, %d]", kMaxTailC);
@@ -846,7 +885,7 @@ int chain_resolve_launch(const float* scores, int64_t cap, int C, const int64_t*
   for (int c = 0; c < C; ++c) tl.l[c] = layers[c];
   // plain launch (full dependency): a conditional graph node may follow it
   const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_limit + 255) / 256, 148));
-  chain_resolve_kernel<<<nb, 256, 0, stream>>>(scores, cap, C, tl, theta, n_dev, n_limit, row_idx,
+  chain_resolve_kernel<<<nb, 256, 0, stream>>>(scores, cap, C, tl, theta, n_dev, n_min, n_limit, row_idx,
                                                exit_layers, tail_count, cond);
   return check_launch("chain_resolve_kernel");
 }

@@ -270,6 +270,7 @@ class _ChainGraphs:
         import os
         e = os.environ
         return tuple(e.get(k) for k in ("TIDE_CHAIN_TAIL", "TIDE_TAIL_AFTER", "TIDE_TAIL_ROWS",
+                                        "TIDE_TAIL_WIDE",
                                         "TIDE_TAIL_KS", "TIDE_SPLIT", "TIDE_PDL",
                                         "TIDE_F32_TAIL_ROWS"))
 
@@ -368,8 +369,6 @@ def select_exits(hidden_states, bank, config: RuntimeConfig, *, n_rows=None,
 
 
 _decode_calls = D.register_cache(D.IdentityCache(64))
-
-
 def _bottleneck(bank, ckpts) -> int:
     if hasattr(bank, "bottleneck"):
         return bank.bottleneck
@@ -452,15 +451,25 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
     rem = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
     cnt = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(2)]
     row_idx, n_dev = 0, 0
-    # Chain tail: after TAIL_AFTER links, the rows still live are scored against
-    # every remaining checkpoint in ONE launch (when few enough: n_limit) and
-    # the remaining links become no-ops — the later links of a peeling chain
-    # hold a handful of rows each, so per-link latency, not bytes, is their cost.
+    # Chain tails score the rows still live against every remaining
+    # checkpoint in ONE launch (a row's score at checkpoint k depends only on
+    # that row, so the first firing checkpoint is what peeling computes):
+    #  * WIDE, right after the first link, for high thresholds (rare exits:
+    #    peeling would read almost every remaining capture anyway, one
+    #    latency-bound link at a time): one cluster per live tile and
+    #    checkpoint, whatever the live count; no links follow;
+    #  * SMALL, after TAIL_AFTER links: taken when at most n_limit rows are
+    #    left (the later links of a peeling chain hold a handful of rows, so
+    #    per-link latency, not bytes, is their cost).  When it handled the
+    #    rows it sets the live count the following links read to 0 (they take
+    #    the idle path; under graph capture they sit in a conditional node
+    #    the tail switches off).
+    tails = _tail_enabled() and code != N.F32
+    wide_at = 0 if (tails and len(ckpts) >= 3 and _tail_wide(theta)) else -1
     after = _tail_after()
-    tail_at = after - 1 if (code != N.F32 and len(ckpts) - after >= 2
-                            and _tail_enabled()) else -1
-    ls = s  # stream the links go to (a graph conditional's body after the tail)
-    body = None
+    tail_at = after - 1 if (tails and len(ckpts) - after >= 2) else -1
+    ls = s  # stream the links go to (a graph conditional's body after a tail)
+    bodies = []
     for i, k in enumerate(ckpts):
         wd, wu = device_weights(bank.routers[k], code, dev)
         h = staged[k + 1]
@@ -470,12 +479,20 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
                                cnt[i & 1].data_ptr(), ws, ls), "tide_route")
         row_idx = rem[i & 1].data_ptr()
         n_dev = cnt[i & 1].data_ptr() + 8
-        if i == tail_at:
-            n_dev, body = _chain_tail(lib, staged, bank, ckpts[i + 1:], code, dev, n, d, b, eps,
-                                      theta, row_idx, n_dev, exit_layers, ws, s)
+        if i == wide_at or i == tail_at:
+            rest = ckpts[i + 1:]
+            if i == wide_at:
+                if _chain_tail(lib, staged, bank, rest, code, dev, n, d, b, eps, theta, row_idx,
+                               n_dev, exit_layers, ws, ls, 0, n, want_cond=False)[0] is None:
+                    break  # launched: it scores every live row, no links follow
+                continue
+            n_dev, body = _chain_tail(lib, staged, bank, rest, code, dev, n, d, b, eps, theta,
+                                      row_idx, n_dev, exit_layers, ws, ls, 0,
+                                      _small_tail_rows(n, d))
             if body is not None:
+                bodies.append(body)
                 ls = body.value
-    if body is not None:
+    for body in reversed(bodies):
         N.check(lib.tide_capture_cond_close(body), "tide_capture_cond_close")
     return exit_layers
 
@@ -498,28 +515,54 @@ def _tail_after() -> int:
     return int(os.environ.get("TIDE_TAIL_AFTER", TAIL_AFTER))
 
 
-def _chain_tail(lib, staged, bank, rest, code, dev, n, d, b, eps, theta, row_idx, n_dev,
-                exit_layers, ws, s):
-    """tide_route_tail over the remaining checkpoints; returns the live-count
-    pointer the following links read (0 rows when the tail handled them)."""
+WIDE_THETA = 0.9  # thresholds from which the chain scores speculatively after link 1
+
+
+def _tail_wide(theta: float) -> bool:
+    """Wide tail after the first link?  Taken for thresholds >= WIDE_THETA:
+    a router fires there only for confident rows, so few rows leave at each
+    checkpoint and speculative scoring reads about what peeling would, in one
+    launch instead of one latency-bound link per checkpoint (measured on
+    configs 2 / 5 at theta = 1.0: 0.23 -> 0.13 ms / 1.47 -> 0.72 ms; at
+    theta <= 0.85 peeling + the small tail is as fast or faster, DESIGN.md
+    §3).  TIDE_TAIL_WIDE=1 / 0 forces it on / off."""
     import os
-    n_limit = int(min(n, max(128, int(os.environ.get("TIDE_TAIL_ROWS", 2048)) * 4096 // d)))
+    env = os.environ.get("TIDE_TAIL_WIDE")
+    if env is not None:
+        return env == "1"
+    return theta >= WIDE_THETA
+
+
+def _small_tail_rows(n: int, d: int) -> int:
+    import os
+    return int(min(n, max(128, int(os.environ.get("TIDE_TAIL_ROWS", 2048)) * 4096 // d)))
+
+
+def _chain_tail(lib, staged, bank, rest, code, dev, n, d, b, eps, theta, row_idx, n_dev,
+                exit_layers, ws, s, n_min, n_limit, want_cond=True):
+    """tide_route_tail_ex over the remaining checkpoints on stream s; returns
+    (the live-count pointer the following links read — 0 rows when the tail
+    handled them —, the conditional body stream under graph capture or None);
+    (None, None) for a launched tail with want_cond=False (nothing follows)."""
     wts = [device_weights(bank.routers[k], code, dev) for k in rest]
     scratch = torch.empty(len(rest) * n, dtype=torch.float32, device=dev)
     tail_count = torch.empty(1, dtype=torch.int64, device=dev)
     # inside CUDA-graph capture the remaining links go into a conditional node
     # that the tail switches off when it handled the rows (no idle launches)
     cond = ctypes.c_uint64(0)
-    if torch.cuda.is_current_stream_capturing():
+    if want_cond and torch.cuda.is_current_stream_capturing():
         N.check(lib.tide_capture_cond_create(s, ctypes.byref(cond)), "tide_capture_cond_create")
-    rc = lib.tide_route_tail(
+    rc = lib.tide_route_tail_ex(
         N.ptr_array([staged[k + 1].data_ptr() for k in rest]), len(rest), d, n, d, code, row_idx,
-        n_dev, n, n_limit, N.ptr_array([w.data_ptr() for w, _ in wts]),
+        n_dev, n, n_min, n_limit, N.ptr_array([w.data_ptr() for w, _ in wts]),
         N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(rest), eps, theta,
         scratch.data_ptr(), exit_layers.data_ptr(), tail_count.data_ptr(), cond.value, ws, s)
     if rc:
         return n_dev, None  # shape without a split-K plan: the links do the work
-    _chain_tail.keep = (scratch, tail_count)  # alive until the stream reaches them
+    # alive until the stream reaches them (stream-ordered allocator reuse)
+    _chain_tail.keep = getattr(_chain_tail, "keep", ())[-4:] + (scratch, tail_count)
+    if not want_cond:
+        return None, None
     body = None
     if cond.value:
         body = ctypes.c_void_p()

@@ -251,14 +251,17 @@ def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch)
         exc |= np.abs(t - O.logit_of(theta)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
     want = O.first_exit_from_scores(scores, theta)
     out = {}
-    for tail in ("1", "0"):
+    # wide tail right after link 1 / links + small tail / plain links
+    for wide, tail in (("1", "1"), ("0", "1"), ("0", "0")):
+        monkeypatch.setenv("TIDE_TAIL_WIDE", wide)
         monkeypatch.setenv("TIDE_CHAIN_TAIL", tail)
         got = P.select_exits(states, bank, cfg).cpu().numpy()
-        assert np.all((got == want) | exc), tail
-        out[tail] = got
-    assert np.all((out["1"] == out["0"]) | exc)
+        assert np.all((got == want) | exc), (wide, tail)
+        out[wide + tail] = got
+    assert np.all((out["11"] == out["00"]) | exc)
+    assert np.all((out["01"] == out["00"]) | exc)
     if theta == 1.0:
-        assert np.all(out["1"] == P.NO_EXIT)
+        assert all(np.all(v == P.NO_EXIT) for v in out.values())
 
 
 @pytest.mark.parametrize("variant", [{"TIDE_DECODE_CLUSTER": "0"}, {"TIDE_DECODE_TMA": "0"},
@@ -283,11 +286,13 @@ def test_decode_step_fallback_paths(variant, monkeypatch):
 
 @pytest.mark.parametrize("d,n,L,scale,theta", [(4096, 4096, 32, 0.1, 0.5), (4096, 1000, 24, 0.2, 1.0),
                                                (8192, 2048, 40, 0.06, 0.7)])
-def test_chain_captured_in_cuda_graph(d, n, L, scale, theta):
-    """select_exits captured in a CUDA graph (the links after the chain tail
-    sit in a conditional node the tail switches off) == eager, on replays with
-    new capture contents."""
+@pytest.mark.parametrize("wide", ["1", "0"])
+def test_chain_captured_in_cuda_graph(d, n, L, scale, theta, wide, monkeypatch):
+    """select_exits captured in a CUDA graph (link 1 + the wide tail, or the
+    links with the ones after the small chain tail in a conditional node the
+    tail switches off) == eager, on replays with new capture contents."""
     need_gpu()
+    monkeypatch.setenv("TIDE_TAIL_WIDE", wide)
     ckpts, routers, states, bank, head = _big_case(L, d, n, "bf16", 90 + n, scale=scale)
     cfg = P.RuntimeConfig(exit_threshold=theta)
     s = torch.cuda.Stream()

@@ -173,6 +173,39 @@ def training(n=65_536, d=4096, epochs=2):
             "rows_per_s": n * epochs / sec, "accuracy": st.accuracy}
 
 
+def lm_head(n=4096, d=4096, V=50257):
+    """§8f-1: posthoc_select's LM head on tcgen05 (3 bf16 MMA terms, f32-grade)
+    at GPT-2's vocabulary, against the f32 library GEMM it replaced."""
+    from paper_2603_21365_b200 import _device as Dv
+    from paper_2603_21365_b200 import _native as N
+    from paper_2603_21365_b200.runtime import split_bf16
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(8)
+    a = torch.randn((n, d), generator=gen, device="cuda")
+    w = torch.randn((V, d), generator=gen, device="cuda") * 0.02
+    ah, al = split_bf16(a, d)
+    bh, bl = split_bf16(w, d)
+    ldo = (V + 3) // 4 * 4
+    out = torch.empty((n, ldo), dtype=torch.float32, device="cuda")
+    lib = N.load()
+    s = Dv.stream_handle(torch.device("cuda", 0))
+
+    def run(terms):
+        return lambda: lib.tide_lm_head(ah.data_ptr(), al.data_ptr() if terms == 3 else None, d, n,
+                                        d, bh.data_ptr(), bl.data_ptr() if terms == 3 else None,
+                                        d, V, out.data_ptr(), ldo, s)
+    ms3 = _time(run(3), reps=10)
+    ms1 = _time(run(1), reps=10)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    ms_lib = _time(lambda: a @ w.t(), reps=3, warm=1)
+    flop = 2.0 * n * V * d
+    return {"config": f"LM head (f8-1): logits [{n} x {V}] = rows [{n} x {d}] . W^T, f32-grade",
+            "ms_3term": ms3, "tflops_3term_bf16_mma": 3 * flop / (ms3 / 1e3) / 1e12,
+            "tflops_3term_f32_equiv": flop / (ms3 / 1e3) / 1e12,
+            "ms_1term_bf16": ms1, "tflops_1term": flop / (ms1 / 1e3) / 1e12,
+            "ms_torch_f32_sgemm": ms_lib, "speedup_3term_vs_sgemm": ms_lib / ms3}
+
+
 def chain_sweep():
     """Peeling-chain configs 2 and 5 across thresholds, down to the worst case
     theta = 1.0 where no row ever exits and every link routes every row."""
@@ -184,7 +217,7 @@ def run_extra(dev=None):
     out = []
     for fn in (config1, config2, config3,
                lambda: config3(P.BATCH_UNANIMOUS), lambda: config3(dtype=torch.float16),
-               config5, config4, training):
+               config5, config4, lm_head, training):
         try:
             out.append(fn())
         except Exception as e:  # report, do not hide
@@ -195,7 +228,9 @@ def run_extra(dev=None):
 if __name__ == "__main__":
     import json
     import sys
-    if len(sys.argv) > 1 and sys.argv[1] == "sweep":
+    if len(sys.argv) > 1 and sys.argv[1] == "lm":
+        print(json.dumps(lm_head()), flush=True)
+    elif len(sys.argv) > 1 and sys.argv[1] == "sweep":
         for r in chain_sweep():
             print(json.dumps(r), flush=True)
     else:

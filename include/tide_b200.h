@@ -122,6 +122,30 @@ int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int
                  void* cont_rows, int64_t* counts, void* workspace, void* stream);
 
 /*
+ * The LM head of posthoc_select (ee/model.py:329-338, ee/runtime.py:176-181:
+ * logits = final_norm(rows) @ lm_head^T) on the tensor cores:
+ *   out[n, V] (f32, leading dim ld_out) = A[n, d] . B[V, d]^T
+ * with A, B as bf16 pairs (x = hi + lo, lo = bf16(x - bf16(x))): three MMA
+ * terms hi.hi + hi.lo + lo.hi, f32 accumulation (small terms apart) — f32-grade
+ * logits.  a_lo = b_lo = NULL: hi only (bf16 products).  ld_a, ld_b
+ * multiples of 8 (any d <= ld), ld_out a multiple of 4, 16-byte aligned
+ * pointers.
+ */
+int tide_lm_head(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, int32_t d,
+                 const void* b_hi, const void* b_lo, int64_t ld_b, int64_t V, float* out,
+                 int64_t ld_out, void* stream);
+
+/*
+ * select_project writing the LM head's A operand directly: every row final-
+ * normed in f32 exactly as tide_select_project computes it, stored as the
+ * bf16 pair hi = bf16(y), lo = bf16(y - hi) ([n, d] each, leading dim ld_out).
+ */
+int tide_select_project_split(const void* const* layer_ptrs, int32_t num_ptrs, int64_t ld_h,
+                              int32_t dtype, const int64_t* exit_layers, int64_t n, int32_t d,
+                              const float* gain, float eps, void* out_hi, void* out_lo,
+                              int64_t ld_out, void* stream);
+
+/*
  * u8 exit codes for the multi-GPU exit-map exchange (the
  * reference's exit map is ee/runtime.py:153-178's int64 exit_layers):
  * code[i] = exit_layers[i] + 1, so NO_EXIT (-1) -> 0 and checkpoint k -> k+1

@@ -42,6 +42,10 @@ SIGNATURES = {
                                      _i32, _c_p, _c_p, _c_p, ctypes.c_uint32, _c_p]),
     "tide_compact": (ctypes.c_int, [_c_p, _i64, _c_p, _c_p, _i32, _c_p, _i64, _i32, _i32, _c_p,
                                     _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "tide_lm_head": (ctypes.c_int, [_c_p, _c_p, _i64, _i64, _i32, _c_p, _c_p, _i64, _i64, _c_p,
+                                    _i64, _c_p]),
+    "tide_select_project_split": (ctypes.c_int, [ctypes.POINTER(_c_p), _i32, _i64, _i32, _c_p,
+                                                 _i64, _i32, _c_p, _f32, _c_p, _c_p, _i64, _c_p]),
     "tide_exit_encode": (ctypes.c_int, [_c_p, _i64, _c_p, _c_p]),
     "tide_exit_decode": (ctypes.c_int, [_c_p, _i64, _c_p, _c_p]),
     "tide_exit_project": (ctypes.c_int, [_c_p, _i64, _i32, _c_p, _i64, _c_p, _i32, _c_p, _f32,

@@ -266,6 +266,25 @@ int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
+int tide_lm_head(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, int32_t d,
+                 const void* b_hi, const void* b_lo, int64_t ld_b, int64_t V, float* out,
+                 int64_t ld_out, void* stream) {
+  if (n < 0 || V < 0 || d < 1 || !a_hi || !b_hi || (n > 0 && V > 0 && !out))
+    return set_error(TIDE_ERR_ARG, "tide_lm_head: bad arguments");
+  if ((a_lo == nullptr) != (b_lo == nullptr))
+    return set_error(TIDE_ERR_ARG, "tide_lm_head: give both lo operands or neither");
+  if (ld_a % 8 || ld_b % 8 || ld_a < d || ld_b < d || ld_out % 4 || ld_out < V)
+    return set_error(TIDE_ERR_UNSUPPORTED,
+                     "tide_lm_head: ld_a, ld_b multiples of 8 (>= d); ld_out a multiple of 4 (>= V)");
+  const uintptr_t al = reinterpret_cast<uintptr_t>(a_hi) | reinterpret_cast<uintptr_t>(a_lo) |
+                       reinterpret_cast<uintptr_t>(b_hi) | reinterpret_cast<uintptr_t>(b_lo) |
+                       reinterpret_cast<uintptr_t>(out);
+  if (al & 15) return set_error(TIDE_ERR_ARG, "tide_lm_head: pointers must be 16-byte aligned");
+  if (n == 0 || V == 0) return TIDE_OK;
+  return lmhead_launch(a_hi, a_lo, ld_a, n, d, b_hi, b_lo, ld_b, V, out, ld_out,
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
 int tide_exit_encode(const int64_t* exit_layers, int64_t n, uint8_t* code, void* stream) {
   if (n < 0 || (n > 0 && (!exit_layers || !code)))
     return set_error(TIDE_ERR_ARG, "tide_exit_encode: bad arguments");

@@ -67,6 +67,9 @@ int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const i
                    int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
                    int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,
                    void* cont_rows, int64_t* counts, void* workspace, cudaStream_t stream);
+int lmhead_launch(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, int32_t d,
+                  const void* b_hi, const void* b_lo, int64_t ld_b, int64_t V, float* out,
+                  int64_t ld_out, cudaStream_t stream);
 int exit_code_launch(const int64_t* layers, int64_t n, uint8_t* code, int decode,
                      cudaStream_t stream);
 

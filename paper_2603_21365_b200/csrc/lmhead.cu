@@ -1,0 +1,230 @@
+// K8: the LM head of posthoc_select on tcgen05 (ee/model.py:329-338,
+// ee/runtime.py:176-181: logits = final_norm(rows) @ lm_head^T in f32).
+//
+//   out[n, V] = A[n, d] . B[V, d]^T
+//
+// A = the final-normed rows select_project stages, B = the LM head, both
+// given as bf16 pairs x = hi + lo (hi = bf16(x), lo = bf16(x - hi): x to
+// ~2^-17 relative).  Three kind::f16 MMAs per K step give f32-grade products:
+//   acc_big   += A_hi B_hi                 (TMEM columns [0, 256))
+//   acc_small += A_hi B_lo + A_lo B_hi     (TMEM columns [256, 512))
+// The two small terms accumulate apart from the big one, so their low bits
+// are not lost against a large running sum; the epilogue adds them once.
+// (lo pointers NULL: one MMA per step, bf16 products.)
+//
+// Tile 128 rows x 256 vocab columns per CTA, K chunks of 64 (the 128-byte
+// swizzle atom), TMA into a 2-stage ring of 96 KB (A_hi, A_lo 16 KB each,
+// B_hi, B_lo 32 KB each), one MMA-issuing warp, 4 epilogue warps draining
+// TMEM (32 columns at a time) into f32 rows.  Grid x = row tiles (fastest),
+// y = vocab tiles: the row tiles of one vocab tile run in the same wave, so
+// each 256-row slice of the LM head is read from HBM once and from L2 by the
+// others (A, all rows hi + lo, stays L2-resident).  Roofline: tensor —
+// 2 n V d flop per term; the 3-term form runs 3 MMAs per step.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tide {
+
+namespace {
+
+constexpr int kLThreads = 192;
+constexpr int kLBM = 128, kLBN = 256, kLBK = 64;
+constexpr uint32_t kLASlot = kLBM * 128;  // 16 KB
+constexpr uint32_t kLBSlot = kLBN * 128;  // 32 KB
+
+struct LmParams {
+  int64_t n, V, ld_out;
+  int32_t nk, stages, terms;
+  uint32_t stage_bytes, idesc;
+  float* out;
+};
+
+template <int kTerms>
+__global__ void __launch_bounds__(kLThreads, 1)
+    lmhead_kernel(const __grid_constant__ CUtensorMap tm_ah, const __grid_constant__ CUtensorMap tm_al,
+                  const __grid_constant__ CUtensorMap tm_bh, const __grid_constant__ CUtensorMap tm_bl,
+                  const __grid_constant__ LmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 8;
+  uint64_t* acc_full = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * kLBM, v0 = (int64_t)blockIdx.y * kLBN;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_ah);
+    prefetch_tmap(&tm_bh);
+    if (kTerms == 3) {
+      prefetch_tmap(&tm_al);
+      prefetch_tmap(&tm_bl);
+    }
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, kTerms == 3 ? 512u : 256u);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // the staged rows may come from the kernel just before on the stream
+  griddep_wait();
+
+  if (warp == 0) {
+    // ----------------------------------------------------------- producer
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();   // A is re-read by every vocab tile
+      const uint64_t pol_b = policy_evict_first();  // a B slice serves one wave of row tiles
+      const uint32_t bytes = kTerms == 3 ? 2u * (kLASlot + kLBSlot) : kLASlot + kLBSlot;
+      for (int kc = 0; kc < p.nk; ++kc) {
+        const int s = kc % p.stages;
+        mbar_wait(&empty[s], ((kc / p.stages) & 1) ^ 1);
+        uint8_t* st = smem + (size_t)s * p.stage_bytes;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_load_2d(st, &tm_ah, &full[s], kc * kLBK, (int)m0, pol_a);
+        tma_load_2d(st + kLASlot, &tm_bh, &full[s], kc * kLBK, (int)v0, pol_b);
+        if (kTerms == 3) {
+          tma_load_2d(st + kLASlot + kLBSlot, &tm_al, &full[s], kc * kLBK, (int)m0, pol_a);
+          tma_load_2d(st + 2 * kLASlot + kLBSlot, &tm_bl, &full[s], kc * kLBK, (int)v0, pol_b);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ----------------------------------------------------------- MMA issuer
+    const uint64_t dh = sw128_kmajor_desc(0);
+    for (int kc = 0; kc < p.nk; ++kc) {
+      const int s = kc % p.stages;
+      mbar_wait(&full[s], (kc / p.stages) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint8_t* st = smem + (size_t)s * p.stage_bytes;
+        const uint64_t ah = dh | (uint64_t)((smem_u32(st) & 0x3FFFFu) >> 4);
+        const uint64_t bh = dh | (uint64_t)((smem_u32(st + kLASlot) & 0x3FFFFu) >> 4);
+        const uint64_t al = dh | (uint64_t)((smem_u32(st + kLASlot + kLBSlot) & 0x3FFFFu) >> 4);
+        const uint64_t bl = dh | (uint64_t)((smem_u32(st + 2 * kLASlot + kLBSlot) & 0x3FFFFu) >> 4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t acc = (kc != 0 || k != 0) ? 1u : 0u;
+          tc_mma_f16(tmem_base, ah + 2 * k, bh + 2 * k, p.idesc, acc);
+          if (kTerms == 3) {
+            tc_mma_f16(tmem_base + 256u, ah + 2 * k, bl + 2 * k, p.idesc, acc);
+            tc_mma_f16(tmem_base + 256u, al + 2 * k, bh + 2 * k, p.idesc, 1u);
+          }
+        }
+        tc_commit(&empty[s]);
+        if (kc == p.nk - 1) tc_commit(acc_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quadrant
+    const int64_t row = m0 + 32 * q + lane;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16);
+    float* orow = p.out + row * p.ld_out;
+    for (int c0 = 0; c0 < kLBN; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(taddr + (uint32_t)c0, v);
+      tmem_ld_wait_regs(v);
+      if (kTerms == 3) {
+        uint32_t w[32];
+        tmem_ld32(taddr + 256u + (uint32_t)c0, w);
+        tmem_ld_wait_regs(w);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+      }
+      if (row < p.n) {
+        const int64_t col = v0 + c0;
+        if (col + 32 <= p.V) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(orow + col + j) =
+                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                            __uint_as_float(v[j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col + j < p.V) orow[col + j] = __uint_as_float(v[j]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTerms == 3 ? 512u : 256u);
+  }
+}
+
+}  // namespace
+
+int lmhead_launch(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, int32_t d,
+                  const void* b_hi, const void* b_lo, int64_t ld_b, int64_t V, float* out,
+                  int64_t ld_out, cudaStream_t stream) {
+  const int terms = (a_lo && b_lo) ? 3 : 1;
+  CUtensorMap ah, al, bh, bl;
+  int rc;
+  if ((rc = make_map(&ah, a_hi, TIDE_BF16, d, n, ld_a, kLBK, kLBM))) return rc;
+  if ((rc = make_map(&bh, b_hi, TIDE_BF16, d, V, ld_b, kLBK, kLBN))) return rc;
+  if (terms == 3) {
+    if ((rc = make_map(&al, a_lo, TIDE_BF16, d, n, ld_a, kLBK, kLBM))) return rc;
+    if ((rc = make_map(&bl, b_lo, TIDE_BF16, d, V, ld_b, kLBK, kLBN))) return rc;
+  } else {
+    al = ah;
+    bl = bh;
+  }
+  LmParams p{};
+  p.n = n;
+  p.V = V;
+  p.ld_out = ld_out;
+  p.nk = (d + kLBK - 1) / kLBK;
+  p.terms = terms;
+  p.stage_bytes = terms == 3 ? 2u * (kLASlot + kLBSlot) : kLASlot + kLBSlot;
+  const uint32_t cap = 227u * 1024u - 1024u - 256u;
+  p.stages = (int)std::min<uint32_t>(8u, cap / p.stage_bytes);
+  p.idesc = f16_idesc(1, kLBM, kLBN);
+  p.out = out;
+  const uint32_t smem = (uint32_t)p.stages * p.stage_bytes + 256u + 1024u;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lmhead_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(lmhead_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  const int64_t gy = (V + kLBN - 1) / kLBN;
+  if (gy > 65535) return set_error(TIDE_ERR_UNSUPPORTED, "tide_lm_head: vocab too large (%lld)", (long long)V);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((n + kLBM - 1) / kLBM), (unsigned)gy, 1);
+  cfg.blockDim = dim3(kLThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr1[1];
+  attr1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr1[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr1;
+  cfg.numAttrs = 1;
+  const cudaError_t e = terms == 3 ? cudaLaunchKernelEx(&cfg, lmhead_kernel<3>, ah, al, bh, bl, p)
+                                   : cudaLaunchKernelEx(&cfg, lmhead_kernel<1>, ah, al, bh, bl, p);
+  if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "lmhead_kernel: %s", cudaGetErrorString(e));
+  return check_launch("lmhead_kernel");
+}
+
+}  // namespace tide

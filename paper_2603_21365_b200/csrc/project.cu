@@ -109,6 +109,24 @@ __device__ __forceinline__ void norm_row(const T* __restrict__ src, float* __res
   }
 }
 
+// The same row as norm_row, written as a bf16 pair y = hi + lo (hi = bf16(y),
+// lo = bf16(y - hi)): the A operand of the 3-term tensor-core LM head.
+template <typename T>
+__device__ __forceinline__ void norm_row_split(const T* __restrict__ src, __nv_bfloat16* __restrict__ hi,
+                                               __nv_bfloat16* __restrict__ lo, int d,
+                                               const float* __restrict__ gain, float eps) {
+  const int lane = threadIdx.x & 31;
+  const float ss = np_pairwise_sumsq<T>(src, d);
+  const float den = __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps));
+  for (int k = lane; k < d; k += 32) {
+    float y = __fdiv_rn(to_f32<T>(src[k]), den);
+    if (gain) y = __fmul_rn(y, gain[k]);
+    const __nv_bfloat16 h = __float2bfloat16_rn(y);
+    hi[k] = h;
+    lo[k] = __float2bfloat16_rn(y - __bfloat162float(h));  // y - h is exact in f32
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kPThreads)
     exit_project_kernel(const T* rows, int64_t ld_rows, const int64_t* src_idx, int64_t n_e_host,
@@ -133,6 +151,8 @@ struct SelectParams {
   const float* gain;
   float eps;
   float* out;
+  __nv_bfloat16* out_hi;  // split mode (out == NULL): bf16 pair rows, leading dim ld_out
+  __nv_bfloat16* out_lo;
 };
 
 template <typename T>
@@ -146,7 +166,10 @@ __global__ void __launch_bounds__(kPThreads) select_project_kernel(const __grid_
       if (k != TIDE_NO_EXIT && k + 1 >= 0 && k + 1 < p.num) src = k + 1;
     }
     const T* row = reinterpret_cast<const T*>(p.layer[src]) + i * p.ld_h;
-    norm_row<T>(row, p.out + i * p.ld_out, p.d, p.gain, p.eps, 1);
+    if (p.out_hi)
+      norm_row_split<T>(row, p.out_hi + i * p.ld_out, p.out_lo + i * p.ld_out, p.d, p.gain, p.eps);
+    else
+      norm_row<T>(row, p.out + i * p.ld_out, p.d, p.gain, p.eps, 1);
   }
 }
 
@@ -193,11 +216,35 @@ extern "C" int tide_exit_project(const void* rows, int64_t ld_rows, int32_t dtyp
   return check_launch("exit_project_kernel");
 }
 
+static int select_project_impl(const void* const* layer_ptrs, int32_t num_ptrs, int64_t ld_h,
+                               int32_t dtype, const int64_t* exit_layers, int64_t n, int32_t d,
+                               const float* gain, float eps, float* out, __nv_bfloat16* out_hi,
+                               __nv_bfloat16* out_lo, int64_t ld_out, void* stream);
+
 extern "C" int tide_select_project(const void* const* layer_ptrs, int32_t num_ptrs, int64_t ld_h,
                                    int32_t dtype, const int64_t* exit_layers, int64_t n,
                                    int32_t d, const float* gain, float eps, float* out,
                                    int64_t ld_out, void* stream) {
-  if (num_ptrs < 1 || num_ptrs > kMaxPtrs || d < 1 || n < 0 || !out || !layer_ptrs ||
+  if (!out) return set_error(TIDE_ERR_ARG, "tide_select_project: bad arguments");
+  return select_project_impl(layer_ptrs, num_ptrs, ld_h, dtype, exit_layers, n, d, gain, eps, out,
+                             nullptr, nullptr, ld_out, stream);
+}
+
+extern "C" int tide_select_project_split(const void* const* layer_ptrs, int32_t num_ptrs,
+                                         int64_t ld_h, int32_t dtype, const int64_t* exit_layers,
+                                         int64_t n, int32_t d, const float* gain, float eps,
+                                         void* out_hi, void* out_lo, int64_t ld_out, void* stream) {
+  if (!out_hi || !out_lo) return set_error(TIDE_ERR_ARG, "tide_select_project_split: null output");
+  return select_project_impl(layer_ptrs, num_ptrs, ld_h, dtype, exit_layers, n, d, gain, eps,
+                             nullptr, reinterpret_cast<__nv_bfloat16*>(out_hi),
+                             reinterpret_cast<__nv_bfloat16*>(out_lo), ld_out, stream);
+}
+
+static int select_project_impl(const void* const* layer_ptrs, int32_t num_ptrs, int64_t ld_h,
+                               int32_t dtype, const int64_t* exit_layers, int64_t n, int32_t d,
+                               const float* gain, float eps, float* out, __nv_bfloat16* out_hi,
+                               __nv_bfloat16* out_lo, int64_t ld_out, void* stream) {
+  if (num_ptrs < 1 || num_ptrs > kMaxPtrs || d < 1 || n < 0 || ld_out < d || !layer_ptrs ||
       !layer_ptrs[num_ptrs - 1])
     return set_error(TIDE_ERR_ARG, "tide_select_project: bad arguments");
   if (n == 0) return TIDE_OK;
@@ -212,6 +259,8 @@ extern "C" int tide_select_project(const void* const* layer_ptrs, int32_t num_pt
   p.gain = gain;
   p.eps = eps;
   p.out = out;
+  p.out_hi = out_hi;
+  p.out_lo = out_lo;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int grid = grid_for(n);
   switch (dtype) {

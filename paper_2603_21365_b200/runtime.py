@@ -12,8 +12,9 @@
     firing checkpoint is exactly what peeling computes);
   * batch-unanimous, n > 16: one launch per checkpoint until all rows fire;
   * then one select_project launch final-norms every row from its exit layer
-    (exit_projection + the final-rows rmsnorm of ee/runtime.py:176,180) and
-    cuBLAS multiplies by the LM head.
+    (exit_projection + the final-rows rmsnorm of ee/runtime.py:176,180) into
+    the bf16-pair operand of the tensor-core LM head (tide_lm_head, 3 MMA
+    terms, f32-grade logits).
 
 `model` is anything with .config.num_layers, .config.hidden_dim, .final_norm
 and .lm_head — the reference's ReferenceModel, or `OutputHead` below.  `bank`
@@ -31,7 +32,7 @@ import torch
 
 from . import _device as D
 from . import _native as N
-from .router_ops import _NoTF32, device_weights
+from .router_ops import device_weights
 from .tensor_math import DEFAULT_EPS
 
 PER_TOKEN = "per-token"
@@ -114,7 +115,24 @@ class OutputHead:
 _head_cache = D.register_cache(D.IdentityCache(4))
 
 
+def _pad8(d: int) -> int:
+    return (d + 7) // 8 * 8
+
+
+def split_bf16(x: torch.Tensor, ld: int):
+    """f32 [r, d] -> bf16 pair (hi, lo) [r, ld] (zero-padded columns): hi =
+    bf16(x), lo = bf16(x - hi); x - hi is exact in f32, so x = hi + lo to
+    ~2^-17 relative (the B operand of tide_lm_head)."""
+    r, d = x.shape
+    hi = torch.zeros((r, ld), dtype=torch.bfloat16, device=x.device)
+    lo = torch.zeros((r, ld), dtype=torch.bfloat16, device=x.device)
+    hi[:, :d] = x.to(torch.bfloat16)
+    lo[:, :d] = (x - hi[:, :d].float()).to(torch.bfloat16)
+    return hi, lo
+
+
 def _device_head(model, dev):
+    """(final-norm gain f32 [d], LM head as the bf16 pair (hi, lo) [vocab, ld])."""
     key = (id(model), dev.index)
     fn, lm = model.final_norm, model.lm_head
     owners = (model, fn, lm)
@@ -123,7 +141,37 @@ def _device_head(model, dev):
         return hit
     g = D.to_device_f32(fn, dev).reshape(-1)
     w = D.to_device_f32(lm, dev)
-    return _head_cache.put(key, owners, (g, w))
+    hi, lo = split_bf16(w, _pad8(w.shape[1]))
+    del w
+    return _head_cache.put(key, owners, (g, hi, lo))
+
+
+def lm_head_logits(staged_ptrs, dtype_code, exit_layers, n, d, gain, w_hi, w_lo, dev, s,
+                   eps=DEFAULT_EPS):
+    """select_project (every row final-normed from its exit layer, written as
+    the bf16 pair) + the tensor-core LM head: logits [n, vocab] f32."""
+    lib = N.load()
+    V = w_hi.shape[0]
+    ld = w_hi.shape[1]
+    a_hi = torch.empty((n, ld), dtype=torch.bfloat16, device=dev)
+    a_lo = torch.empty((n, ld), dtype=torch.bfloat16, device=dev)
+    if ld != d:
+        a_hi[:, d:].zero_()
+        a_lo[:, d:].zero_()
+    logits = torch.empty((n, _pad4(V)), dtype=torch.float32, device=dev)
+    if n:
+        N.check(lib.tide_select_project_split(
+            N.ptr_array(staged_ptrs), len(staged_ptrs), d, dtype_code, exit_layers.data_ptr(), n,
+            d, gain.data_ptr(), float(np.float32(eps)), a_hi.data_ptr(), a_lo.data_ptr(), ld, s),
+            "tide_select_project_split")
+        N.check(lib.tide_lm_head(a_hi.data_ptr(), a_lo.data_ptr(), ld, n, d, w_hi.data_ptr(),
+                                 w_lo.data_ptr(), ld, V, logits.data_ptr(), logits.shape[1], s),
+                "tide_lm_head")
+    return logits[:, :V] if logits.shape[1] != V else logits
+
+
+def _pad4(v: int) -> int:
+    return (v + 3) // 4 * 4
 
 
 def _check_bank(model, hidden_states, bank) -> None:
@@ -652,18 +700,12 @@ def posthoc_select(model, hidden_states, bank, config: RuntimeConfig, *,
         exit_layers = select_exits(hidden_states, bank, config, staged=staged, dev=dev)
     logits = None
     if return_logits:
-        gain, lm = _device_head(model, dev)
-        normed = torch.empty((n, d), dtype=torch.float32, device=dev)
+        gain, w_hi, w_lo = _device_head(model, dev)
         ptrs = [0] * len(hidden_states)
         for i, t in staged.items():
             ptrs[i] = t.data_ptr()
-        if n:
-            N.check(N.load().tide_select_project(
-                N.ptr_array(ptrs), len(ptrs), d, D.dtype_code(final), exit_layers.data_ptr(), n,
-                d, gain.data_ptr(), float(np.float32(DEFAULT_EPS)), normed.data_ptr(), d,
-                D.stream_handle(dev)), "tide_select_project")
-        with _NoTF32():
-            logits = normed @ lm.t()
+        logits = lm_head_logits(ptrs, D.dtype_code(final), exit_layers, n, d, gain, w_hi, w_lo,
+                                dev, D.stream_handle(dev))
     if host:
         return (D.to_host(logits) if logits is not None else None), D.to_host(exit_layers)
     return logits, exit_layers

@@ -9,7 +9,10 @@ ONLY the checkpoint layers' outputs and the final one, and expose them with
 the reference's indexing, so `posthoc_select(model, capture.hidden_states,
 bank, cfg)` works unchanged.  With `online=True` the fused router runs inside
 the hook for each checkpoint as soon as its layer output exists (same stream,
-peeling chain on device), so the exit map is ready when the forward returns.
+peeling chain on device), so the exit map is ready when the forward returns;
+decode-sized batches (<= 16 rows) are routed in ONE decode-kernel launch when
+the last checkpoint's output exists (tools/hook_bench.py: ~1 us of a
+6 ms batch-8 decode step; the per-checkpoint links cost ~58 us there).
 
 The decoder layer list is resolved like the reference's structure adapter
 (ee/adapter.py:26-32 named paths, then the largest module list).
@@ -54,6 +57,14 @@ class _Placeholder:
         self.shape = tuple(shape)
 
 
+def _decode_rows() -> int:
+    """Batches up to this many rows are routed in one decode-kernel launch
+    (TIDE_HOOK_DECODE=0: per-checkpoint links at every size)."""
+    import os
+    from . import _native as N
+    return N.MAX_DECODE_ROWS if os.environ.get("TIDE_HOOK_DECODE", "1") != "0" else 0
+
+
 def _rows(out) -> torch.Tensor:
     t = out[0] if isinstance(out, (tuple, list)) else out
     return t.reshape(-1, t.shape[-1])
@@ -93,6 +104,8 @@ class CheckpointCapture:
         self._caps: dict = {}
         self.exit_layers = None
         self._chain = None
+        routed = [k for k in self.checkpoints if config is None or k >= config.k_min]
+        self._last_routed = routed[-1] if routed else -1
 
     # -- capture ------------------------------------------------------------
     def _hook(self, k):
@@ -102,7 +115,14 @@ class CheckpointCapture:
                 rows = rows.float()
             self._caps[k + 1] = rows
             if self.online and k in self.checkpoints and k >= self.config.k_min:
-                self._route_online(k, rows)
+                if rows.shape[0] <= _decode_rows():
+                    # decode-sized batch: one launch for every checkpoint once
+                    # the last one exists (a per-checkpoint link at 8 rows is
+                    # a whole launch for a few KB)
+                    if k == self._last_routed:
+                        self._route_decode()
+                else:
+                    self._route_online(k, rows)
         return fn
 
     def _new_forward(self, module, inputs):
@@ -141,6 +161,17 @@ class CheckpointCapture:
         return out
 
     # -- online routing (per-token peeling chain, no host sync) -------------
+    def _route_decode(self):
+        """All routed checkpoints of a decode-sized batch in one launch (the
+        decode kernel: per-token first firing checkpoint, in-kernel)."""
+        from .runtime import select_exits
+        staged = {k + 1: self._caps[k + 1].contiguous() for k in self.checkpoints
+                  if k >= self.config.k_min}
+        final = staged[self._last_routed + 1]
+        staged[self.bank.num_layers] = final  # only its shape is read on this path
+        self.exit_layers = select_exits(None, self.bank, self.config, staged=staged,
+                                        dev=final.device)
+
     def _route_online(self, k, rows):
         import numpy as np
 

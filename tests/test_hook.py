@@ -76,3 +76,38 @@ def test_online_routing_equals_posthoc():
     offline = P.select_exits(cap.hidden_states, bank, cfg).cpu().numpy()
     np.testing.assert_array_equal(online, offline)
     assert (online >= 0).any() and (online < 0).any()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,shape", [(torch.bfloat16, (8, 512)), (torch.float16, (3, 700)),
+                                         (torch.bfloat16, (8, 1)), (torch.float32, (4, 300))])
+def test_online_routing_matches_oracle(dtype, shape):
+    """Online routing inside the layer hooks (link per checkpoint as the
+    forward runs; decode-sized batches too) == the oracle's first-exit map of
+    the captured checkpoint rows (ee/runtime.py:151-178 per-token, band rule of
+    SURVEY.md §8c) — the oracle, not the CUDA path, is the reference here."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from tests.gpu_helpers import RTOL
+    d, L = 256, 12
+    m = Tiny(L, d).cuda().to(dtype)
+    g = np.random.Generator(np.random.PCG64(5))
+    routers = {k: O.make_router(d, 128, k, g, scale=0.2) for k in (3, 7, 11)}
+    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L)
+    theta = 0.55
+    cfg = P.RuntimeConfig(exit_threshold=theta)
+    x = torch.randn(*shape, d, device="cuda").to(dtype)
+    with torch.no_grad(), CheckpointCapture(m, bank.checkpoints, bank=bank, config=cfg,
+                                            online=True) as cap:
+        m(x)
+    got = cap.exit_layers.cpu().numpy()
+    hs = cap.hidden_states
+    scores, exc = {}, np.zeros(got.shape[0], bool)
+    tol = RTOL["f32" if dtype == torch.float32 else "bf16"]
+    for k, r in routers.items():
+        s, t, mm = O.route_logits(hs[k + 1].float().cpu().numpy(), r)
+        scores[k] = s
+        exc |= np.abs(t - O.logit_of(theta)) <= tol * np.maximum(np.abs(t), mm)
+    want = O.first_exit_from_scores(scores, theta)
+    assert np.all((got == want) | exc), int(((got != want) & ~exc).sum())
+    assert exc.mean() < 0.5  # the band does not excuse everything

@@ -15,9 +15,11 @@ NCCL).  Inputs are 512 MiB per step, larger than the 126 MB L2, so no flush.
 selection over 20 checkpoints at d=8192, u8 exit-code all-gather) and 4
 (calibration labeller + count all-reduce), weak or strong scaling.
 
-`--impl reference` times the reference algorithm on the host cores instead
-(the oracle port of ee/router_ops.py:68-87 + ee/runtime.py:171 +
-ee/router_ops.py:137-154, token-sharded over worker processes).
+`--impl reference` times the reference on the host cores instead: the
+UNMODIFIED earlyexit functions (ee/router_ops.py:68-87 fused_layernorm_route,
+the strict mask of ee/runtime.py:171, ee/router_ops.py:137-154 batch_compact)
+from baseline/_ref when staged there (tools/stage_reference.py), else the
+oracle port of the same loop; token-sharded over one process per core.
 """
 
 from __future__ import annotations
@@ -153,21 +155,54 @@ def ncu_traffic(kernel: str):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference / baseline (oracle port, token-sharded over processes)
+# CPU reference / baseline: the UNMODIFIED reference functions when the
+# reference package is staged in baseline/_ref (tools/stage_reference.py;
+# git-ignored, travels to the GPU box), else the oracle port of the same loop
 # ---------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _have_reference() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "earlyexit"))
+
+
 def _cpu_worker(args):
-    seed, rows, d, b = args
+    """One worker = one host core: route + strict mask + stable compaction of a
+    token shard with the reference's own functions (ee/router_ops.py:68-87,
+    ee/runtime.py:171, ee/router_ops.py:137-154)."""
+    seed, rows, d, b, kind = args
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    from oracle import tide_oracle as O
+    from oracle import tide_oracle as O  # seeded weights / rows only
     g = np.random.Generator(np.random.PCG64(202))
-    router = O.make_router(d, b, 3, g)
+    orouter = O.make_router(d, b, 3, g)
     rng = np.random.Generator(np.random.PCG64(seed))
     h = O.round_to(rng.standard_normal((rows, d), dtype=np.float32), "bf16")
+    if kind == "reference":
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from earlyexit import router_ops as R
+        router = R.Router(layer=3, w_down=orouter.w_down, w_up=orouter.w_up)
+        route, compact = R.fused_layernorm_route, R.batch_compact
+    else:
+        router, route, compact = orouter, O.fused_layernorm_route, O.batch_compact
     t0 = time.perf_counter()
-    scores = O.fused_layernorm_route(h, router)           # ee/router_ops.py:68-87
-    mask = scores > np.float32(THETA)                     # ee/runtime.py:171
-    O.batch_compact(h, mask)                              # ee/router_ops.py:137-154
-    return rows, time.perf_counter() - t0
+    scores = route(h, router)                   # ee/router_ops.py:68-87
+    mask = scores > np.float32(THETA)           # ee/runtime.py:171
+    t1 = time.perf_counter()
+    compact(h, mask)                            # ee/router_ops.py:137-154
+    t2 = time.perf_counter()
+    return rows, t2 - t0, t2 - t1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class CpuReference:
@@ -177,24 +212,54 @@ class CpuReference:
     def __init__(self, cores=None):
         import multiprocessing as mp
         self.cores = cores or os.cpu_count() or 1
+        self.kind = "reference" if _have_reference() else "port"
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         self.pool = mp.get_context("spawn").Pool(self.cores)
-        rows, dt = self.pool.map(_cpu_worker, [(7, 128, D, B)] * self.cores)[0]
+        rows, dt, _ = self.pool.map(_cpu_worker, [(7, 128, D, B, self.kind)] * self.cores)[0]
         self.per_proc = rows / max(dt, 1e-9)
 
     def sample(self, target_s: float) -> dict:
         rows_each = int(max(64, min(65536, self.per_proc * target_s)))
         rows_each = int(math.ceil(rows_each / 64) * 64)
-        res = self.pool.map(_cpu_worker, [(100 + i, rows_each, D, B) for i in range(self.cores)])
-        total = sum(r for r, _ in res)
-        slowest = max(t for _, t in res)
-        return {"value": total / slowest, "unit": UNIT, "cores": self.cores, "kind": "port",
+        res = self.pool.map(_cpu_worker, [(100 + i, rows_each, D, B, self.kind)
+                                          for i in range(self.cores)])
+        total = sum(r for r, _, _ in res)
+        slowest = max(t for _, t, _ in res)
+        compact_share = sum(c for _, _, c in res) / max(1e-9, sum(t for _, t, _ in res))
+        what = ("unmodified earlyexit 0.1.0 from baseline/_ref" if self.kind == "reference"
+                else "oracle port of the reference loop")
+        return {"value": total / slowest, "unit": UNIT, "cores": self.cores, "kind": self.kind,
                 "sample": f"{self.cores} processes x {rows_each} tokens (d=4096, bf16-rounded "
-                          f"rows as f32; per-row reference loop + strict mask + batch_compact)",
-                "tokens": total, "seconds": slowest}
+                          f"rows as f32; {what}: fused_layernorm_route + strict mask + "
+                          f"batch_compact, whose row copy is {100 * compact_share:.1f}% of the "
+                          f"time)",
+                "tokens": total, "seconds": slowest, "cpu_model": cpu_model()}
 
     def close(self):
         self.pool.terminate()
+
+
+def cpu_single_process_rates(target_s: float = 3.0) -> dict:
+    """The reference on ONE process: OPENBLAS_NUM_THREADS=1 and =nproc (the
+    reference's own BLAS threading for its per-row matvecs), in subprocesses
+    so the thread count takes effect."""
+    out = {}
+    kind = "reference" if _have_reference() else "port"
+    for threads in (1, os.cpu_count() or 1):
+        code = ("import sys, json, time; sys.path.insert(0, %r); import bench; "
+                "r, t, _ = bench._cpu_worker((5, 256, bench.D, bench.B, %r)); "
+                "n = max(256, int(256 * %f / max(t, 1e-9)) // 64 * 64); "
+                "r, t, _ = bench._cpu_worker((6, n, bench.D, bench.B, %r)); "
+                "print(json.dumps({'tokens': r, 'seconds': t}))") % (ROOT, kind, target_s, kind)
+        env = dict(os.environ, OPENBLAS_NUM_THREADS=str(threads), OMP_NUM_THREADS=str(threads))
+        try:
+            r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                               text=True, timeout=300)
+            j = json.loads(r.stdout.strip().splitlines()[-1])
+            out[f"one_process_blas_threads_{threads}"] = j["tokens"] / j["seconds"]
+        except Exception as e:  # report, do not hide
+            out[f"one_process_blas_threads_{threads}"] = f"failed: {e!r}"[:200]
+    return out
 
 
 def cpu_reference_rate(target_s: float = 10.0) -> dict:
@@ -222,7 +287,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": workload_config(max(1, args.gpus)), "impl": "reference",
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": runs[-1]["cores"],
-                             "kind": "port", "sample": runs[-1]["sample"]},
+                             "kind": runs[-1]["kind"], "sample": runs[-1]["sample"],
+                             "cpu_model": runs[-1]["cpu_model"]},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -460,7 +526,8 @@ def run_ours(args):
         if not args.no_cpu_baseline and world == 1:  # the host baseline: rank 0 at N = 1
             line["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(
                 float(os.environ.get("TIDE_CPU_BASELINE_S", "10"))).items()
-                if k in ("value", "unit", "cores", "kind", "sample")}
+                if k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+            line["cpu_baseline"].update(cpu_single_process_rates())
         if args.extra:
             from bench_extra import run_extra
             line["extra"]["configs"] = run_extra(dev)

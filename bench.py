@@ -141,8 +141,10 @@ def measured_peaks() -> dict:
     if os.path.exists(p):
         with open(p) as fh:
             d = json.load(fh)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+        return {"hbm_gbs": float(d["hbm_gbs"]),
+                "bf16_tflops": float(d.get("bf16_tflops", 1590.0)),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
 
 
 def ncu_traffic(kernel: str):
@@ -528,6 +530,12 @@ def run_ours(args):
                 float(os.environ.get("TIDE_CPU_BASELINE_S", "10"))).items()
                 if k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
             line["cpu_baseline"].update(cpu_single_process_rates())
+        if world == 1 and not args.no_configs:
+            # BASELINE configs 1-5 (+ the worst-case thresholds and the LM head)
+            # timed in the same run, each with its roofline fraction
+            from bench_extra import run_configs
+            pk = measured_peaks()
+            line["configs"] = run_configs(pk["hbm_gbs"], pk["bf16_tflops"])
         if args.extra:
             from bench_extra import run_extra
             line["extra"]["configs"] = run_extra(dev)
@@ -730,6 +738,8 @@ def main():
     ap.add_argument("--extra", action="store_true", help="also time configs 2-5 (slower)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the BASELINE configs 1-5 block of the N=1 line")
     ap.add_argument("--config", default="headline", choices=["headline", "4", "5"],
                     help="headline (BASELINE metric), or the sharded config-4 / config-5 legs")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],

@@ -213,6 +213,27 @@ def chain_sweep():
             + [config5(t) for t in (0.7, 0.85, 1.0)])
 
 
+def run_configs(hbm_gbs: float, bf16_tflops: float):
+    """The BASELINE configs timed inside the driver's default bench run (N=1),
+    each with its roofline fraction: HBM for the streaming paths (algorithmic
+    / peeled bytes), bf16 tensor peak for the LM head."""
+    out = []
+    for fn in (config1, lambda: config2(0.5), lambda: config2(1.0), config3, config4,
+               lambda: config5(0.7), lambda: config5(1.0), lm_head):
+        try:
+            r = fn()
+        except Exception as e:  # report, do not hide
+            out.append({"error": repr(e)[:300]})
+            continue
+        for k in ("gbs_graph", "gbs"):
+            if k in r:
+                r["hbm_frac"] = r[k] / hbm_gbs
+        if "tflops_3term_bf16_mma" in r:
+            r["tensor_frac_3term"] = r["tflops_3term_bf16_mma"] / bf16_tflops
+        out.append(r)
+    return out
+
+
 def run_extra(dev=None):
     out = []
     for fn in (config1, config2, config3,

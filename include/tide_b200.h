@@ -55,8 +55,10 @@ int tide_sm_count(int device);
 size_t tide_workspace_bytes(void);
 int tide_workspace_init(void* workspace, void* stream);
 
-/* 1 when (dtype, d, b) runs on the tcgen05 tensor-core kernel, else 0 (the
- * CUDA-core kernel handles f32 and every other shape). */
+/* 1 when (dtype, d, b) runs on a tcgen05 tensor-core kernel for large row
+ * counts, else 0.  bf16 / f16: route_tc (all row counts).  f32: the 3xTF32
+ * kernel for d <= 8192 from 16,384 rows (within the 1e-5 f32 contract); fewer
+ * rows and other shapes take the CUDA-core kernel (f32 products). */
 int tide_route_uses_tensor_cores(int32_t dtype, int32_t d, int32_t b);
 
 /*

@@ -63,7 +63,7 @@ int tide_workspace_init(void* workspace, void* stream) {
 }
 
 int tide_route_uses_tensor_cores(int32_t dtype, int32_t d, int32_t b) {
-  if (dtype == TIDE_F32) return route_tf32_supported(d, b) ? 1 : 0;
+  if (dtype == TIDE_F32) return route_tf32_supported(d, b, 1 << 30) ? 1 : 0;
   return route_tc_supported(dtype, d, b) ? 1 : 0;
 }
 
@@ -132,7 +132,7 @@ int tide_route_ex(const void* h, int64_t ld_h, int64_t n, const int64_t* n_dev,
   if (route_tc_supported(dtype, d, b) && aligned) return route_tc_launch(a, s);
   // f32 rows: the 3xTF32 tensor-core kernel (route_tf32.cu) where its error
   // bound holds and the rows are 16-byte aligned for TMA, else CUDA cores
-  if (dtype == TIDE_F32 && route_tf32_supported(d, b) && ld_h % 4 == 0 &&
+  if (dtype == TIDE_F32 && route_tf32_supported(d, b, n) && ld_h % 4 == 0 &&
       ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(w_down)) & 15) == 0)
     return route_tf32_launch(a, s);
   return route_simt_launch(a, s);

@@ -61,7 +61,7 @@ int chain_resolve_launch(const float* scores, int64_t cap, int C, const int64_t*
                          float theta, const int64_t* n_dev, int64_t n_min, int64_t n_limit,
                          const int64_t* row_idx, int64_t* exit_layers, int64_t* tail_count,
                          unsigned long long cond, cudaStream_t stream);
-bool route_tf32_supported(int d, int b);
+bool route_tf32_supported(int d, int b, int64_t n);
 int route_tf32_launch(const RouteArgs& a, cudaStream_t stream);
 int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
                    int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,

@@ -67,6 +67,7 @@ struct TfParams {
   const int64_t* n_dev;
   int64_t rows_total;
   int32_t d, b, npad, bp, tpg, nk, na, nl, nw, nx;
+  int32_t nacc;  // TMEM accumulators per tile: 1, 2 (hi.hi | small terms), 4 (each by k-chunk parity)
   uint32_t idesc, tmem_cols, wslot, whalf;
   uint32_t off_a, off_l, off_wup, off_bar, off_words, off_ids, off_tmem;
   const int64_t* row_idx;
@@ -275,12 +276,22 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
           const uint64_t al =
               desc_hi | (uint64_t)((smem_u32(sL + (size_t)ls * kTfSlot) & 0x3FFFFu) >> 4);
           const uint64_t bl = bdesc + wlo_step;
-          const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
+          // accumulators of this tile: big (hi.hi) and small (lo.hi + hi.lo),
+          // each split by k-chunk parity when nacc = 4 — every accumulator
+          // sees a fraction of the MMA steps, and the tensor core's per-step
+          // loss of low accumulator bits (a bias toward zero that grows with
+          // the number of steps) shrinks in proportion
+          const uint32_t tb = tmem_base + (uint32_t)(t * p.nacc * p.bp);
+          const int par = p.nacc == 4 ? (kc & 1) : 0;
+          const uint32_t d_big = tb + (uint32_t)(par * p.bp);
+          const uint32_t d_small = p.nacc == 1 ? d_big : tb + (uint32_t)((p.nacc / 2 + par) * p.bp);
+          const bool first = kc < (p.nacc == 4 ? 2 : 1);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            tc_mma_tf32(dt, ax + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
-            tc_mma_tf32(dt, al + 2 * k, bdesc + 2 * k, p.idesc, 1u);
-            tc_mma_tf32(dt, ax + 2 * k, bl + 2 * k, p.idesc, 1u);
+            tc_mma_tf32(d_big, ax + 2 * k, bdesc + 2 * k, p.idesc, (first && k == 0) ? 0u : 1u);
+            tc_mma_tf32(d_small, al + 2 * k, bdesc + 2 * k, p.idesc,
+                        (p.nacc != 1 && first && k == 0) ? 0u : 1u);
+            tc_mma_tf32(d_small, ax + 2 * k, bl + 2 * k, p.idesc, 1u);
           }
           tc_commit(&a_empty[as]);
           if (kc == p.nk - 1) tc_commit(&t_full[t]);
@@ -388,11 +399,21 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
           const float sq = (acc_ss[0] + acc_ss[1]) + (acc_ss[2] + acc_ss[3]);
           const float scale = rms_scale(sq, p.inv_d, p.eps);
           float tl = 0.0f;
-          const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(t * p.bp);
+          const uint32_t taddr =
+              tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(t * p.nacc * p.bp);
           for (int c0 = 0; c0 < p.b; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(taddr + (uint32_t)c0, v);
             tmem_ld_wait_regs(v);
+            // the other accumulators of the tile: (big1) + small0 (+ small1)
+            for (int ai = 1; ai < p.nacc; ++ai) {
+              uint32_t w[32];
+              tmem_ld32(taddr + (uint32_t)(ai * p.bp + c0), w);
+              tmem_ld_wait_regs(w);
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj)
+                v[jj] = __float_as_uint(__uint_as_float(v[jj]) + __uint_as_float(w[jj]));
+            }
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj)
               if (c0 + jj < p.b)
@@ -511,23 +532,52 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
   if (threadIdx.x == 0) launch_done(p.ws);
 }
 
-// Opt-in (TIDE_F32_TC=1): the tensor core's f32 accumulation drops low bits
-// on every MMA step, a bias that grows with d — measured max |dt|/max(|t|,m)
-// 4e-6 at d = 768 but 2.2e-5 at d = 4096, outside the 1e-5 f32 contract — so
-// the CUDA-core kernel (f32 FMAs, 1e-6) stays the default for f32 rows.
-bool route_tf32_supported(int d, int b) {
+// Accumulators per tile.  The tensor core's f32 accumulation drops low bits on
+// every MMA step, a bias toward zero that grows with the number of steps: with
+// every term in one accumulator, max |dt|/max(|t|,m) was 4e-6 at d = 768 but
+// 2.2e-5 at d = 4096, outside the 1e-5 f32 contract.  Four accumulators
+// (hi.hi and the small terms apart, each split by k-chunk parity) give every
+// accumulator 1/2 of the steps and keep the big sum free of the 2/3 of MMAs
+// that carry small terms.  TIDE_TF32_ACC = 1 / 2 / 4 overrides (read per call).
+// Measured max |dt|/max(|t|,m) on B200 (tools/tf32_probe.py, rows N(0,9)):
+//   d      768     4096    8192    16384
+//   acc 1  4.0e-6  2.2e-5  4.3e-5  8.9e-5
+//   acc 2  1.4e-6  7.1e-6  1.4e-5  2.9e-5
+//   acc 4  8.5e-7  3.5e-6  7.2e-6  1.4e-5
+// so 2 accumulators (2 tiles per group) up to d = 4096 and 4 (1 tile per
+// group: W re-read per tile) up to d = 8192 stay inside the 1e-5 contract.
+int tf32_nacc(int d, int nk) {
+  const char* env = getenv("TIDE_TF32_ACC");
+  int v = env ? atoi(env) : (d <= 4096 ? 2 : 4);
+  if (v != 1 && v != 2 && v != 4) v = 4;
+  if (v == 4 && nk < 2) v = 2;
+  return v;
+}
+
+// f32 rows on tcgen05 (TIDE_F32_TC=0 forces the CUDA-core kernel, =1 this one
+// at any shape): the default for d <= kTf32MaxD and n >= kTf32MinRows.  Below
+// that row count every CTA re-reads and re-splits all of W for a few rows
+// (W-bound: 0.24 ms at 4,096 x 4096, as the CUDA-core kernel); at 65,536 x 4096
+// 0.57 ms against 1.82 ms on CUDA cores.
+constexpr int kTf32MaxD = 8192;
+constexpr int64_t kTf32MinRows = 16384;
+bool route_tf32_supported(int d, int b, int64_t n) {
   const char* env = getenv("TIDE_F32_TC");  // read per call: tests switch it
-  if (!env || env[0] != '1') return false;
-  return d >= 4 && d % 4 == 0 && b >= 1 && b <= 128;
+  if (env && env[0] == '0') return false;
+  const bool forced = env && env[0] == '1';
+  return d >= 4 && d % 4 == 0 && b >= 1 && b <= 128 &&
+         (forced || (d <= kTf32MaxD && n >= kTf32MinRows));
 }
 
 int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
   const int npad = (a.b + 15) / 16 * 16;
   const int bp = (npad + 31) / 32 * 32;
-  const int tpg = std::min(4, 512 / bp);
-  int cols = 32;
-  while (cols < tpg * bp) cols <<= 1;
   const int nk = (a.d + 31) / 32;
+  const int nacc = tf32_nacc(a.d, nk);
+  const int tpg = std::max(1, std::min(4, 512 / (bp * nacc)));
+  if (tpg * bp * nacc > 512) return set_error(TIDE_ERR_UNSUPPORTED, "tf32: TMEM too small");
+  int cols = 32;
+  while (cols < tpg * bp * nacc) cols <<= 1;
   const uint32_t whalf = (uint32_t)npad * 128u;
   const uint32_t wslot = 2 * whalf;
   const int nw = kTfMaxNW;
@@ -547,6 +597,7 @@ int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
   p.npad = npad;
   p.bp = bp;
   p.tpg = tpg;
+  p.nacc = nacc;
   p.nk = nk;
   p.na = na;
   p.nl = nl;

@@ -33,7 +33,10 @@ FILES = ["test_router_ops.py", "test_runtime.py", "test_tensor_math.py", "test_c
 # `rmsnorm(h) @ lm_head.T` (ee/model.py:338), i.e. with the summation order
 # of the host's OpenBLAS sgemm kernel (which even changes with the matrix
 # shape on one CPU).  The exit maps the same tests assert come first and pass;
-# the logits differ by ~1 ulp, which the check below bounds (MAX_LOGIT_ULP_ABS).
+# the logits come from the tensor-core LM head (tide_lm_head: three bf16 MMA
+# terms, |error| <= 1e-5 * sum_j |a_j w_j|, tests/test_gpu_lmhead.py) and differ
+# from OpenBLAS by ~1e-6 on the reference's desk model (d = 64, |a_j w_j| sum
+# ~1), which the check below bounds (MAX_LOGIT_ABS).
 _LOGITS_BITWISE = ("asserts np.testing.assert_array_equal(logits, lm_head_from_hidden(...)): "
                    "bit-equality with the host BLAS sgemm summation order")
 EXPECTED_FAILURES = {
@@ -43,7 +46,7 @@ EXPECTED_FAILURES = {
     "TestPosthocSelect::test_hot_layer_exits_everything[per-token]": _LOGITS_BITWISE,
     "TestPosthocSelect::test_hot_layer_exits_everything[batch-unanimous]": _LOGITS_BITWISE,
 }
-MAX_LOGIT_ULP_ABS = 1e-6
+MAX_LOGIT_ABS = 1e-5
 
 
 def _outcomes(xml_path):
@@ -94,10 +97,10 @@ def test_reference_suite_through_shim(tmp_path):
     unexpected = [k for k in summary["failed"] if k not in EXPECTED_FAILURES]
     for k in summary["failed"]:
         if k in EXPECTED_FAILURES:
-            # only the bitwise logits assertion failed, by at most ~1 ulp
+            # only the bitwise logits assertion failed, inside the LM head contract
             m = re.search(r"Max absolute difference among violations: ([0-9.eE+-]+)",
                           summary["messages"][k])
-            if not m or float(m.group(1)) > MAX_LOGIT_ULP_ABS:
+            if not m or float(m.group(1)) > MAX_LOGIT_ABS:
                 unexpected.append(k)
     assert not unexpected, json.dumps({k: summary["messages"][k] for k in unexpected},
                                       indent=1)[:6000]

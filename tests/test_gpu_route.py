@@ -95,7 +95,8 @@ def test_tensor_core_path_selected():
     lib = N.load()
     assert lib.tide_route_uses_tensor_cores(N.BF16, 4096, 128) == 1
     assert lib.tide_route_uses_tensor_cores(N.F16, 8192, 256) == 1
-    assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 128) == 0
+    assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 128) == 1   # 3xTF32, >= 16,384 rows
+    assert lib.tide_route_uses_tensor_cores(N.F32, 16384, 128) == 0  # outside its 1e-5 range
 
 
 @pytest.fixture(params=["split", "persistent"])
@@ -341,6 +342,48 @@ def test_f32_tensor_core_opt_in(n, d, b, monkeypatch):
     e, c = O.compact_indices(r["mask"].cpu().numpy())
     np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
     np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("n,d,b", [(20000, 4096, 128), (16384, 8192, 128), (65536, 4096, 128),
+                                   (30000, 1000, 96)])
+def test_f32_default_tensor_cores_within_contract(n, d, b):
+    """f32 rows from 16,384 on take the 3xTF32 tcgen05 kernel by default
+    (segmented TMEM accumulators): logits inside the 1e-5 f32 contract at
+    d <= 8192, compaction bit-exact."""
+    need_gpu()
+    assert N.load().tide_route_uses_tensor_cores(N.F32, d, b) == 1
+    g = np.random.Generator(np.random.PCG64(7 * n + d))
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = g.standard_normal((n, d), dtype=np.float32) * 3.0
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, "f32"), _router(wd, wu), theta=0.5, want_logits=True,
+                want_indices=True)
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, "f32", f"tf32 default n={n} d={d}")
+    e, c = O.compact_indices(r["mask"].cpu().numpy())
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
+    np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("acc", ["2", "4"])
+def test_f32_tensor_core_accumulator_layouts(acc, monkeypatch):
+    """The segmented TMEM accumulator layouts (2 / 4 per tile) are inside the
+    f32 contract at d = 2048 (one accumulator is not: 1.06e-5 there) with a
+    bit-exact compaction."""
+    need_gpu()
+    monkeypatch.setenv("TIDE_F32_TC", "1")
+    monkeypatch.setenv("TIDE_TF32_ACC", acc)
+    n, d, b = 5000, 2048, 128
+    g = np.random.Generator(np.random.PCG64(99))
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = g.standard_normal((n, d), dtype=np.float32) * 3.0
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, "f32"), _router(wd, wu), theta=0.5, want_logits=True,
+                want_indices=True)
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, "f32", f"tf32 acc={acc}")
+    e, _ = O.compact_indices(r["mask"].cpu().numpy())
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
 
 
 @pytest.mark.parametrize("dtype,n,d,b", [("f32", 9000, 768, 128), ("f32", 7200, 100, 40),

@@ -46,7 +46,8 @@ def test_library_metadata_without_gpu(lib):
     assert lib.tide_version().decode().startswith("tide_b200")
     assert lib.tide_workspace_bytes() == N.WORKSPACE_BYTES
     assert lib.tide_route_uses_tensor_cores(N.BF16, 4096, 128) == 1
-    assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 128) == 0
+    assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 128) == 1  # 3xTF32 (large n)
+    assert lib.tide_route_uses_tensor_cores(N.F32, 16384, 128) == 0
     assert lib.tide_route_uses_tensor_cores(N.BF16, 4096, 512) == 0
 
 

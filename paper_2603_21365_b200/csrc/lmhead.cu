@@ -87,8 +87,14 @@ __global__ void __launch_bounds__(kLThreads, 1)
   if (warp == 0) {
     // ----------------------------------------------------------- producer
     if (lane == 0) {
-      const uint64_t pol_a = policy_evict_last();   // A is re-read by every vocab tile
-      const uint64_t pol_b = policy_evict_first();  // a B slice serves one wave of row tiles
+      // A (all rows, hi + lo) is re-read by every vocab tile: keep it; a B
+      // slice serves the row tiles of one wave: normal priority.  ncu at
+      // 4096 x 50,257 x 4096: 3.8 GB read from DRAM per launch (B is 0.82 GB,
+      // A 64 MB; evict_first on B measured the same), ~1 TB/s — far from the
+      // bound; the tensor pipe is 71% active (profiles/r02_lmhead_kernel_3term.json)
+      const uint64_t pol_a = policy_evict_last();
+      uint64_t pol_b;
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_b));
       const uint32_t bytes = kTerms == 3 ? 2u * (kLASlot + kLBSlot) : kLASlot + kLBSlot;
       for (int kc = 0; kc < p.nk; ++kc) {
         const int s = kc % p.stages;

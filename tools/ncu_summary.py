@@ -63,6 +63,10 @@ def short(name):
         targ = name.split("<", 1)[1].split(">")[0]
         if base == "route_tc_kernel":
             return base + ("_bf16" if targ.strip() in ("1", "true") else "_f16")
+        if base == "route_tcs_kernel":  # <kBF16, NC>: NC > 1 is the chain tail
+            return base + ("_tail" if targ.split(",")[-1].strip() not in ("1",) else "")
+        if base == "lmhead_kernel":  # <kTerms>
+            return base + "_" + targ.strip() + "term"
     return base
 
 

@@ -55,6 +55,7 @@ struct TcParams {
   const int64_t* n_dev;
   int64_t rows_total;
   int32_t d, b, npad, bp, tpg, nk, na, nw, nx, gran;
+  int32_t pair;  // 1: an A slot holds two tiles (one 256-row TMA box, 32 KB, one barrier cycle)
   uint32_t idesc, tmem_cols, wslot;
   uint32_t off_a, off_wup, off_bar, off_words, off_ids, off_tmem;
   const int64_t* row_idx;
@@ -115,10 +116,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     const __grid_constant__ CUtensorMap tm_h32b,
                     const __grid_constant__ CUtensorMap tm_h32,
                     const __grid_constant__ CUtensorMap tm_w,
-                    const __grid_constant__ CUtensorMap tm_g4, const __grid_constant__ TcParams p) {
+                    const __grid_constant__ CUtensorMap tm_g4,
+                    const __grid_constant__ CUtensorMap tm_h256, const __grid_constant__ TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sW = smem;
+  // pair mode: slot = two tiles' 64-column chunk (rows 0-127: tile 2j, rows
+  // 128-255: tile 2j+1); every RMS warp of both sets reads it
+  const uint32_t slot_bytes = p.pair ? 2u * kASlotBytes : (uint32_t)kASlotBytes;
   uint8_t* sA = smem + p.off_a;
   float* sWup = reinterpret_cast<float*>(smem + p.off_wup);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
@@ -162,14 +167,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_w);
     prefetch_tmap(gathered ? &tm_g4 : &tm_h128);
-    if (!gathered) prefetch_tmap(&tm_h32);
+    if (!gathered) prefetch_tmap(p.pair ? &tm_h256 : &tm_h32);
     for (int i = 0; i < p.nw; ++i) {
       mbar_init(&w_full[i], 1);
       mbar_init(&w_empty[i], 1);
     }
     for (int i = 0; i < p.na; ++i) {
       mbar_init(&a_full[i], 1);
-      mbar_init(&a_empty[i], 1 + 4);  // MMA commit + the 4 RMS warps owning the tile
+      // MMA commit + the 4 RMS warps owning the tile (pair slots: all 8)
+      mbar_init(&a_empty[i], 1 + (p.pair ? 8 : 4));
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&t_full[i], 1);
@@ -216,11 +222,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
           if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
         };
+        auto load_pair = [&](int kc, int pt) {
+          mbar_wait(&a_empty[as], aph ^ 1);
+          uint8_t* dst = sA + (size_t)as * slot_bytes;
+          const int64_t rb = r0 + (int64_t)pt * 256;
+          const bool two = 2 * pt + 1 < T;
+          mbar_arrive_expect_tx(&a_full[as], two ? 2u * kASlotBytes : (uint32_t)kASlotBytes);
+          tma_load_2d(dst, two ? &tm_h256 : &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
+          if (++as == p.na) { as = 0; aph ^= 1; }
+        };
         auto load_a = [&](int kc, int t) {
           const long long q0 = pclk();
           mbar_wait(&a_empty[as], aph ^ 1);
           pw_cyc += pclk() - q0;
-          uint8_t* dst = sA + (size_t)as * kASlotBytes;
+          uint8_t* dst = sA + (size_t)as * slot_bytes;
           const int64_t rb = r0 + (int64_t)t * 128;
           const int rows_in = (int)((r1 - rb) < 128 ? (r1 - rb) : 128);
           if (!gathered) {
@@ -257,18 +272,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         };
         // phase 1 (K-outer): chunk kc's W slot feeds all T tiles
         const int P1 = p.nk - p.nx;
+        const int NP = (T + 1) / 2;
         for (int kc = 0; kc < P1; ++kc) {
           load_w(kc);
-          for (int t = 0; t < T; ++t) load_a(kc, t);
+          if (p.pair)
+            for (int pt = 0; pt < NP; ++pt) load_pair(kc, pt);
+          else
+            for (int t = 0; t < T; ++t) load_a(kc, t);
         }
         // phase 2 (tile-major over the last nx chunks, whose W slots stay
         // resident): tile t's accumulator completes while later tiles still
-        // stream, so its epilogue overlaps the tail of the stream
-        for (int t = 0; t < T; ++t)
-          for (int j = 0; j < p.nx; ++j) {
-            if (t == 0) load_w(P1 + j);
-            load_a(P1 + j, t);
-          }
+        // stream, so its epilogue overlaps the tail of the stream (pair mode:
+        // pair-major, tiles 2j and 2j+1 complete together)
+        if (p.pair) {
+          for (int pt = 0; pt < NP; ++pt)
+            for (int j = 0; j < p.nx; ++j) {
+              if (pt == 0) load_w(P1 + j);
+              load_pair(P1 + j, pt);
+            }
+        } else {
+          for (int t = 0; t < T; ++t)
+            for (int j = 0; j < p.nx; ++j) {
+              if (t == 0) load_w(P1 + j);
+              load_a(P1 + j, t);
+            }
+        }
       }
     }
     if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[18] = pw_cyc; dbg[19] = pclk() - p_begin; }
@@ -294,7 +322,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint64_t adesc =
-              desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * kASlotBytes) & 0x3FFFFu) >> 4);
+              desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * slot_bytes) & 0x3FFFFu) >> 4);
           const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -309,6 +337,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       auto wdesc = [&](int slot) {
         return desc_hi | (uint64_t)((smem_u32(sW + (size_t)slot * p.wslot) & 0x3FFFFu) >> 4);
       };
+      // pair slot: tile 2pt from rows 0-127, tile 2pt+1 from rows 128-255
+      auto mma_pair = [&](int kc, int pt, uint64_t bdesc) {
+        mbar_wait(&a_full[as], aph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t adesc =
+              desc_hi | (uint64_t)((smem_u32(sA + (size_t)as * slot_bytes) & 0x3FFFFu) >> 4);
+          const int nt = (2 * pt + 1 < T) ? 2 : 1;
+          for (int u = 0; u < nt; ++u) {
+            const int t = 2 * pt + u;
+            const uint64_t ad = adesc + (uint64_t)((u * kASlotBytes) >> 4);
+            const uint32_t dt = tmem_base + (uint32_t)(t * p.bp);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(dt, ad + 2 * k, bdesc + 2 * k, p.idesc, (kc | k) != 0);
+            if (kc == p.nk - 1) tc_commit(&t_full[t]);
+          }
+          tc_commit(&a_empty[as]);
+        }
+        __syncwarp();
+        if (++as == p.na) { as = 0; aph ^= 1; }
+      };
+      const int NP = (T + 1) / 2;
       // phase 1: K-outer
       const int P1 = p.nk - p.nx;
       for (int kc = 0; kc < P1; ++kc) {
@@ -316,13 +367,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_wait(&w_full[wsl], wph);
         wait_cyc += pclk() - w0;
         const uint64_t bdesc = wdesc(wsl);
-        for (int t = 0; t < T; ++t) mma_slot(kc, t, bdesc);
+        if (p.pair)
+          for (int pt = 0; pt < NP; ++pt) mma_pair(kc, pt, bdesc);
+        else
+          for (int t = 0; t < T; ++t) mma_slot(kc, t, bdesc);
         if (elect_one()) tc_commit(&w_empty[wsl]);
         __syncwarp();
         if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
       }
       // phase 2: tile-major over the last nx chunks (W slots wsl .. wsl+nx-1)
-      for (int t = 0; t < T; ++t) {
+      if (p.pair) {
+        for (int pt = 0; pt < NP; ++pt) {
+          int sl = wsl, ph = wph;
+          for (int j = 0; j < p.nx; ++j) {
+            if (pt == 0) mbar_wait(&w_full[sl], ph);
+            mma_pair(P1 + j, pt, wdesc(sl));
+            if (pt == NP - 1) {
+              if (elect_one()) tc_commit(&w_empty[sl]);
+              __syncwarp();
+            }
+            if (++sl == p.nw) { sl = 0; ph ^= 1; }
+          }
+        }
+      }
+      for (int t = 0; !p.pair && t < T; ++t) {
         int sl = wsl, ph = wph;
         for (int j = 0; j < p.nx; ++j) {
           if (t == 0) mbar_wait(&w_full[sl], ph);
@@ -361,12 +429,36 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       float ss[2][4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) ss[i][0] = ss[i][1] = ss[i][2] = ss[i][3] = 0.0f;
+      // pair slot: this set's tile is rows [128 wset, 128 wset + 128); a set
+      // whose tile is absent (odd T, last pair) only releases the slot
+      auto rms_pair = [&](int pt, float (&acc)[4]) {
+        mbar_wait(&a_full[as], aph);
+        if (2 * pt + wset < T) {
+          const uint8_t* rp = sA + (size_t)as * slot_bytes + (size_t)wset * kASlotBytes + row * 128;
+          uint4 u[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_empty[as]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            sq2_acc<kBF16>(u[j].x, acc[0], acc[1]);
+            sq2_acc<kBF16>(u[j].y, acc[2], acc[3]);
+            sq2_acc<kBF16>(u[j].z, acc[0], acc[1]);
+            sq2_acc<kBF16>(u[j].w, acc[2], acc[3]);
+          }
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_empty[as]);
+        }
+        if (++as == p.na) { as = 0; aph ^= 1; }
+      };
       auto rms_slot = [&](int t, float (&acc)[4]) {
         if ((t & 1) == wset) {
           const long long s0 = pclk();
           mbar_wait(&a_full[as], aph);
           sw_cyc += pclk() - s0;
-          const uint8_t* rp = sA + (size_t)as * kASlotBytes + row * 128;
+          const uint8_t* rp = sA + (size_t)as * slot_bytes + row * 128;
           uint4 u[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
@@ -384,10 +476,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       };
       // same slot order as the producer: phase 1 K-outer, phase 2 tile-major
       const int P1 = p.nk - p.nx;
+      const int NP = (T + 1) / 2;
       for (int kc = 0; kc < P1; ++kc) {
+        if (p.pair) {
+          for (int pt = 0; pt < NP; ++pt) rms_pair(pt, ss[pt]);
+        } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (t < T) rms_slot(t, ss[t >> 1]);
+          for (int t = 0; t < 4; ++t)
+            if (t < T) rms_slot(t, ss[t >> 1]);
+        }
       }
       const int par = gi & 1;
       mbar_wait(&m_empty[par], (((uint32_t)gi >> 1) & 1u) ^ 1u);
@@ -467,8 +564,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       };
       // phase 2: this set's tiles in completion order; each tile's epilogue
       // runs while the other set's next tile streams
+      if (p.pair) {
+        // pair-major: both sets stream pair 0, then run tiles 0 / 1 at once
+        // while pair 1 streams, then tiles 2 / 3
+        for (int pt = 0; pt < 2; ++pt) {
+          if (pt < NP)
+            for (int j = 0; j < p.nx; ++j) rms_pair(pt, ss[pt]);
+          if (pt == 0 && dbg && warp == 2 && lane == 0) { dbg[2] = gtimer(); }
+          epilogue(2 * pt + wset, ss[pt]);
+        }
+      }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; !p.pair && t < 4; ++t) {
         if (t < T)
           for (int j = 0; j < p.nx; ++j) rms_slot(t, ss[t >> 1]);
         if ((t & 1) == wset) {
@@ -675,7 +782,22 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   const uint32_t off_a = (uint32_t)nw * wslot;
   const int smem_cap = 227 * 1024;
   const uint32_t misc = 1024 /*w_up*/ + 512 /*bars*/ + 128 /*words*/ + 2048 /*ids*/ + 16;
-  int na = (int)((smem_cap - 1024 - off_a - misc) / kASlotBytes);
+  // pair slots (two whole tiles per 32 KB slot: half the barrier round trips
+  // per byte) for dense launches dealt in whole tiles; TIDE_K1_PAIRSLOT=0/1
+  int sms0 = 0;
+  {
+    int dev1 = 0;
+    cudaGetDevice(&dev1);
+    sms0 = sm_count(dev1);
+  }
+  bool pair = a.row_idx == nullptr && a.n_dev == nullptr && a.n % 128 == 0 &&
+              a.n >= (int64_t)sms0 * 256 && tpg == 4;
+  {
+    const char* env = getenv("TIDE_K1_PAIRSLOT");  // read per call
+    if (env) pair = pair && env[0] == '1';
+  }
+  const uint32_t slot_bytes = pair ? 2u * kASlotBytes : (uint32_t)kASlotBytes;
+  int na = (int)((smem_cap - 1024 - off_a - misc) / slot_bytes);
   na = std::min(na, kMaxNA);
   if (na < 2) return set_error(TIDE_ERR_UNSUPPORTED, "bottleneck too wide for smem");
   TcParams p{};
@@ -691,11 +813,12 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.na = na;
   p.nw = nw;
   p.nx = std::min(nw, nk);  // tile-major tail chunks (W slots kept resident)
+  p.pair = pair ? 1 : 0;
   p.idesc = f16_idesc(a.dtype == TIDE_BF16 ? 1 : 0, 128, npad);
   p.tmem_cols = (uint32_t)cols;
   p.wslot = wslot;
   p.off_a = off_a;
-  p.off_wup = off_a + (uint32_t)na * kASlotBytes;
+  p.off_wup = off_a + (uint32_t)na * slot_bytes;
   p.off_bar = p.off_wup + 1024;
   p.off_words = p.off_bar + 512;
   p.off_ids = p.off_words + 128;
@@ -719,7 +842,7 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.ws = reinterpret_cast<Workspace*>(a.workspace);
   p.dbg = g_dbg;
 
-  CUtensorMap tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4;
+  CUtensorMap tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, tm_h256;
   const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
   int rc;
   if ((rc = make_map(&tm_h128, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
@@ -728,6 +851,11 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, kBox))) return rc;
   if ((rc = make_map(&tm_g4, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 1))) return rc;
   if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
+  if (pair) {
+    if ((rc = make_map(&tm_h256, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 256))) return rc;
+  } else {
+    tm_h256 = tm_h128;
+  }
 
   int dev = 0;
   cudaGetDevice(&dev);
@@ -770,9 +898,11 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   }
   cfg.attrs = attr;
   if (a.dtype == TIDE_BF16)
-    cudaLaunchKernelEx(&cfg, route_tc_kernel<true>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
+    cudaLaunchKernelEx(&cfg, route_tc_kernel<true>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4,
+                       tm_h256, p);
   else
-    cudaLaunchKernelEx(&cfg, route_tc_kernel<false>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, p);
+    cudaLaunchKernelEx(&cfg, route_tc_kernel<false>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4,
+                       tm_h256, p);
   return check_launch("route_tc_kernel");
 }
 

@@ -11,7 +11,8 @@ cluster and TMA/tcgen05 protocols of: the persistent tcgen05 router (K1),
 the split-K cluster router (K1s), the peeling chain with its tail + resolve
 kernels, the decode-step kernel, the CUDA-core f32 router, standalone
 compaction with row gather, exit projection / select_project and the
-labeller.
+labeller; round 2: K1's pair slots, the 3xTF32 f32 router, the wide chain
+tail, the tensor-core LM head (via posthoc_select), the exit codec.
 """
 
 import os
@@ -90,8 +91,35 @@ def case_project_label(states, bank, host):
     assert ds is not None
 
 
+def case_round2():
+    """Kernels added in round 2: K1 pair slots (dense whole-tile launch), the
+    f32 3xTF32 route (forced at a small shape), the wide chain tail (theta >=
+    0.9), the exit codec + global compaction (the multi-GPU exchange)."""
+    case_route("0", 38400, 128)          # K1 pair slots: >= 148 x 256 rows, whole tiles
+    os.environ["TIDE_F32_TC"] = "1"
+    case_route("0", 600, 256, torch.float32)   # 3xTF32, segmented accumulators
+    os.environ.pop("TIDE_F32_TC", None)
+    case_chain(700, 256, 24, 0.95)       # link 1 + the wide tail + resolve
+    from paper_2603_21365_b200 import _device as Dv
+    from paper_2603_21365_b200 import _native as N
+    lib = N.load()
+    s = Dv.stream_handle(torch.device("cuda", 0))
+    lay = torch.randint(-1, 30, (5000,), dtype=torch.int64, device="cuda")
+    code = torch.empty(5000, dtype=torch.uint8, device="cuda")
+    N.check(lib.tide_exit_encode(lay.data_ptr(), 5000, code.data_ptr(), s), "encode")
+    idx = torch.empty(5000, dtype=torch.int64, device="cuda")
+    cnt = torch.empty(2, dtype=torch.int64, device="cuda")
+    N.check(lib.tide_compact(code.data_ptr(), 5000, None, None, 0, None, 0, 0, 0, idx.data_ptr(),
+                             None, None, None, cnt.data_ptr(), Dv.workspace().data_ptr(), s),
+            "compact")
+    torch.cuda.synchronize()
+    want = np.flatnonzero(lay.cpu().numpy() >= 0)
+    assert np.array_equal(idx[: int(cnt[0])].cpu().numpy(), want)
+
+
 def main():
     assert torch.cuda.is_available()
+    case_round2()
     case_route("0", 2000, 1024)          # persistent tcgen05 K1 (ragged tail)
     case_route("16", 1000, 2048)         # split-K cluster kernel
     case_route("0", 700, 768, torch.float32)  # CUDA-core f32 router

@@ -61,7 +61,20 @@ def config2(theta=0.5):
                       f"per-token theta={theta}",
             "ms_api": ms, "ms_graph": gms, "tokens_per_s": 4096 / (gms / 1e3),
             "peeled_bytes": peeled, "gbs_graph": peeled / (gms / 1e3) / 1e9,
-            "exit_rate": float((e >= 0).mean()), "launches": len(ckpts)}
+            "exit_rate": float((e >= 0).mean()), **_strategy(ckpts, 4096, 4096, states, theta, gms)}
+
+
+def _strategy(ckpts, n, d, states, theta, gms):
+    """Which chain form select_exits took and the bytes it actually reads:
+    speculative (K1m: every row at every checkpoint, 2 launches) or peeling
+    (one link per checkpoint, live rows only)."""
+    from paper_2603_21365_b200 import runtime as R
+    spec = len(ckpts) <= R.MAX_MULTI_CKPTS and R._speculative(n, d, states[-1], theta)
+    if not spec:
+        return {"strategy": "peeling", "launches": len(ckpts)}
+    read = len(ckpts) * (n * (d * 2 + 4) + 128 * d * 2 + 512)
+    return {"strategy": "speculative (K1m)", "launches": 2, "read_bytes": read,
+            "gbs_read": read / (gms / 1e3) / 1e9}
 
 
 def _graph_time(fn, reps=50, inner=1):
@@ -136,7 +149,7 @@ def config5(theta=0.7):
                       f"per-token theta={theta}",
             "ms_api": ms, "ms_graph": gms, "tokens_per_s": 8192 / (gms / 1e3),
             "peeled_bytes": peeled, "gbs_graph": peeled / (gms / 1e3) / 1e9,
-            "exit_rate": float((e >= 0).mean()), "launches": len(ckpts)}
+            "exit_rate": float((e >= 0).mean()), **_strategy(ckpts, 8192, 8192, states, theta, gms)}
 
 
 def config1():
@@ -228,6 +241,8 @@ def run_configs(hbm_gbs: float, bf16_tflops: float):
         for k in ("gbs_graph", "gbs"):
             if k in r:
                 r["hbm_frac"] = r[k] / hbm_gbs
+        if "gbs_read" in r:
+            r["hbm_frac_read"] = r["gbs_read"] / hbm_gbs
         if "tflops_3term_bf16_mma" in r:
             r["tensor_frac_3term"] = r["tflops_3term_bf16_mma"] / bf16_tflops
         out.append(r)

@@ -309,6 +309,27 @@ int tide_route_tail_ex(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64
                        float theta, float* scores, int64_t* exit_layers, int64_t* tail_count,
                        uint64_t cond_handle, void* workspace, void* stream);
 
+/*
+ * Per-token exit decision over C checkpoints (ee/runtime.py:166-178, the
+ * per-token rule of posthoc_select) in ONE persistent tensor-core launch
+ * plus a resolve step: every row is scored at every checkpoint (speculative:
+ * no peeling between checkpoints) and exit_layers[row id] = layers[first c
+ * whose score > theta]; rows that never fire are left untouched (pre-fill
+ * them with TIDE_NO_EXIT).  Dense (row_idx = n_dev = NULL: rows 0..n-1 of
+ * every capture, row id = row) or gathered (the live rows row_idx[0 ..
+ * *n_dev), n = the list's capacity).  h_ptrs / w_ptrs / wup_ptrs / layers:
+ * HOST arrays of C entries (ascending layers, C <= 24).  scores: device
+ * scratch of C * n f32.  bf16 / f16 rows only.  Same exit map as the
+ * peeling chain (a row's score at a checkpoint depends only on that row).
+ * (No reference counterpart: an execution strategy of posthoc_select.)
+ */
+int tide_route_multi(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n,
+                     const int64_t* n_dev, int64_t rows_total, int32_t d, int32_t dtype,
+                     const int64_t* row_idx, const void* const* w_ptrs,
+                     const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
+                     float theta, float* scores, int64_t* exit_layers, void* workspace,
+                     void* stream);
+
 int tide_capture_cond_create(void* stream, uint64_t* handle);
 int tide_capture_cond_open(void* stream, uint64_t handle, void** body_stream);
 int tide_capture_cond_close(void* body_stream);

@@ -62,6 +62,10 @@ SIGNATURES = {
                                           _c_p, _c_p, _i64, _i64, _i64, ctypes.POINTER(_c_p),
                                           ctypes.POINTER(_c_p), _i32, ctypes.POINTER(_i64), _f32,
                                           _f32, _c_p, _c_p, _c_p, ctypes.c_uint64, _c_p, _c_p]),
+    "tide_route_multi": (ctypes.c_int, [ctypes.POINTER(_c_p), _i32, _i64, _i64, _c_p, _i64, _i32,
+                                        _i32, _c_p, ctypes.POINTER(_c_p), ctypes.POINTER(_c_p),
+                                        _i32, ctypes.POINTER(_i64), _f32, _f32, _c_p, _c_p, _c_p,
+                                        _c_p]),
     "tide_capture_cond_create": (ctypes.c_int, [_c_p, ctypes.POINTER(ctypes.c_uint64)]),
     "tide_capture_cond_open": (ctypes.c_int, [_c_p, ctypes.c_uint64, ctypes.POINTER(_c_p)]),
     "tide_capture_cond_close": (ctypes.c_int, [_c_p]),

@@ -196,6 +196,55 @@ int tide_route_tail_ex(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64
                                (unsigned long long)cond_handle, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int tide_route_multi(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n,
+                     const int64_t* n_dev, int64_t rows_total, int32_t d, int32_t dtype,
+                     const int64_t* row_idx, const void* const* w_ptrs,
+                     const float* const* wup_ptrs, int32_t b, const int64_t* layers, float eps,
+                     float theta, float* scores, int64_t* exit_layers, void* workspace,
+                     void* stream) {
+  if (C < 1 || !h_ptrs || !w_ptrs || !wup_ptrs || !layers)
+    return set_error(TIDE_ERR_ARG, "tide_route_multi: bad checkpoint arrays");
+  if (d < 1 || b < 1 || n < 0 || ld_h < d || (row_idx && rows_total < 1))
+    return set_error(TIDE_ERR_ARG, "tide_route_multi: bad shape");
+  if ((row_idx == nullptr) != (n_dev == nullptr))
+    return set_error(TIDE_ERR_ARG, "tide_route_multi: row_idx and n_dev go together");
+  if (!scores || !exit_layers || !workspace)
+    return set_error(TIDE_ERR_ARG, "tide_route_multi: null device buffer");
+  if ((dtype != TIDE_F16 && dtype != TIDE_BF16) || !route_tc_supported(dtype, d, b) || ld_h % 8)
+    return set_error(TIDE_ERR_UNSUPPORTED, "tide_route_multi: bf16/f16 rows, d %% 8 == 0, b <= 256");
+  for (int c = 0; c < C; ++c)
+    if (((reinterpret_cast<uintptr_t>(h_ptrs[c]) | reinterpret_cast<uintptr_t>(w_ptrs[c])) & 15) ||
+        (c && layers[c] <= layers[c - 1]))
+      return set_error(TIDE_ERR_ARG, "tide_route_multi: unaligned pointer or unordered layers");
+  if (n == 0) return TIDE_OK;
+  RouteArgs a{};
+  a.h = h_ptrs[0];
+  a.ld_h = ld_h;
+  a.n = n;
+  a.n_dev = n_dev;
+  a.rows_total = row_idx ? rows_total : n;
+  a.d = d;
+  a.dtype = dtype;
+  a.row_idx = row_idx;
+  a.w_down = w_ptrs[0];
+  a.w_up = wup_ptrs[0];
+  a.b = b;
+  a.eps = eps;
+  a.theta = theta;
+  a.scores = scores;
+  a.exit_layers = exit_layers;
+  a.workspace = workspace;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int rc;
+  if (C == 1) {  // one checkpoint: the plain route (strict mask -> exit layer)
+    a.layer = layers[0];
+    return route_tc_launch(a, s);
+  }
+  if ((rc = route_tc_multi_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, n, s))) return rc;
+  return chain_resolve_launch(scores, n, C, layers, theta, n_dev, 0, n, row_idx, exit_layers,
+                              nullptr, 0, s);
+}
+
 // --- CUDA-graph conditional for the links after a chain tail -----------------
 int tide_capture_cond_create(void* stream, uint64_t* handle) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -49,6 +49,7 @@ constexpr int kThreadsTC = 352;  // 11 warps: producer, MMA, 2 x 4 epilogue, com
 constexpr int kMaxNA = 16;
 constexpr int kMaxNW = 4;
 constexpr int kASlotBytes = 128 * 128;  // 128 rows x 64 cols x 2 B
+constexpr int kMaxMC = 24;              // checkpoints of one K1m launch
 
 struct TcParams {
   int64_t n_host;
@@ -73,6 +74,49 @@ struct TcParams {
   int64_t* counts;
   Workspace* ws;
   unsigned long long* dbg;  // optional per-CTA timeline (globaltimer ns), 8 slots per CTA
+  // K1m (NC > 1): nc checkpoints in one launch; checkpoint c reads its rows
+  // through MultiMaps::h[c], its router through MultiMaps::w[c] / wups[c] and
+  // writes scores[c * cap + position]; gathered launches route only when
+  // n_min <= *n_dev <= n_limit
+  int32_t nc;
+  int64_t cap, n_min, n_limit;
+  const float* wups[kMaxMC];
+};
+
+// Per-checkpoint tensor maps of a K1m launch (kernel parameters): h[c] is the
+// 128-row box map of capture c (dense) or its 1-row gather4 map (gathered).
+template <int NC>
+struct MultiMaps {
+  CUtensorMap h[NC];
+  CUtensorMap w[NC];
+};
+template <>
+struct MultiMaps<1> {
+  int unused;
+};
+template <int NC>
+__device__ __forceinline__ const CUtensorMap* mm_h(const MultiMaps<NC>& m, int c) {
+  if constexpr (NC > 1) return &m.h[c];
+  else return nullptr;
+}
+template <int NC>
+__device__ __forceinline__ const CUtensorMap* mm_w(const MultiMaps<NC>& m, int c) {
+  if constexpr (NC > 1) return &m.w[c];
+  else return nullptr;
+}
+
+// The groups of rows one CTA walks, in the same order in every role.
+//  NC == 1: groups g = blockIdx.x, + gridDim.x, ... of NG balanced groups of
+//           whole gran-row units (group_range).
+//  NC > 1:  CTA b owns virtual tiles [b TT / G, (b + 1) TT / G) of the
+//           checkpoint-major tile space (TT = nc x Tc, Tc = tiles per
+//           checkpoint); a group is up to tpg consecutive tiles of ONE
+//           checkpoint (its W chunk feeds all of them).
+struct GroupIter {
+  int64_t g, NG, G, n, n32;
+  int gran;
+  int64_t v, vend, Tc;
+  int tpg;
 };
 
 // Cycle counters inside the streaming loops only in profiling builds
@@ -81,6 +125,13 @@ struct TcParams {
 #ifndef TIDE_K1_PROFILE
 #define TIDE_K1_PROFILE 0
 #endif
+#ifndef TIDE_K1_GROUPBAR
+#define TIDE_K1_GROUPBAR 0  // debug: all roles meet at the end of every group
+#endif
+#define K1_GROUP_END()                                                     \
+  do {                                                                     \
+    if (TIDE_K1_GROUPBAR) asm volatile("barrier.sync 1, %0;" ::"r"(kThreadsTC)); \
+  } while (0)
 __device__ __forceinline__ long long pclk() {
 #if TIDE_K1_PROFILE
   return clock64();
@@ -109,7 +160,32 @@ __device__ __forceinline__ void group_range(int64_t g, int64_t n, int64_t nu, in
   if (r1 > n) r1 = n;
 }
 
-template <bool kBF16>
+template <int NC>
+__device__ __forceinline__ bool next_group(GroupIter& it, int& c, int64_t& g, int64_t& r0,
+                                           int64_t& r1) {
+  if constexpr (NC == 1) {
+    if (it.g >= it.NG) return false;
+    c = 0;
+    g = it.g;
+    group_range(it.g, it.n, it.n32, it.NG, it.gran, r0, r1);
+    it.g += it.G;
+    return true;
+  } else {
+    if (it.v >= it.vend) return false;
+    c = (int)(it.v / it.Tc);
+    const int64_t t0 = it.v - (int64_t)c * it.Tc;
+    int64_t t1 = t0 + it.tpg;
+    if (t1 > it.Tc) t1 = it.Tc;
+    if (t1 - t0 > it.vend - it.v) t1 = t0 + (it.vend - it.v);
+    g = it.v;
+    r0 = t0 * 128;
+    r1 = t1 * 128 < it.n ? t1 * 128 : it.n;
+    it.v += t1 - t0;
+    return true;
+  }
+}
+
+template <bool kBF16, int NC>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     route_tc_kernel(const __grid_constant__ CUtensorMap tm_h128,
                     const __grid_constant__ CUtensorMap tm_h64,
@@ -117,7 +193,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     const __grid_constant__ CUtensorMap tm_h32,
                     const __grid_constant__ CUtensorMap tm_w,
                     const __grid_constant__ CUtensorMap tm_g4,
-                    const __grid_constant__ CUtensorMap tm_h256, const __grid_constant__ TcParams p) {
+                    const __grid_constant__ CUtensorMap tm_h256,
+                    const __grid_constant__ MultiMaps<NC> mm, const __grid_constant__ TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sW = smem;
@@ -155,27 +232,50 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const bool dep_inputs = p.n_dev != nullptr || p.row_idx != nullptr || !p.inputs_ready;
   if (dep_inputs) griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
-  const int64_t n = p.n_dev ? *p.n_dev : p.n_host;
+  int64_t n = p.n_dev ? *p.n_dev : p.n_host;
+  if (NC > 1 && p.n_dev && (n < p.n_min || n > p.n_limit)) n = 0;  // K1m tail gate
   const int64_t n32 = (n + p.gran - 1) / p.gran;  // number of gran-row units
   const int64_t G = gridDim.x;
   const int64_t cpg = (int64_t)p.tpg * (128 / p.gran);
   int64_t NG = n32 < G ? n32 : G;
   if ((n32 + cpg - 1) / cpg > NG) NG = (n32 + cpg - 1) / cpg;
   const bool gathered = p.row_idx != nullptr;
-  const bool need_scan = p.exit_idx || p.cont_idx || p.counts;
+  const bool need_scan = NC == 1 && (p.exit_idx || p.cont_idx || p.counts);
+  auto make_iter = [&]() {
+    GroupIter it;
+    it.g = blockIdx.x;
+    it.NG = NG;
+    it.G = G;
+    it.n = n;
+    it.n32 = n32;
+    it.gran = p.gran;
+    it.tpg = p.tpg;
+    it.Tc = (n + 127) / 128;
+    const int64_t TT = (int64_t)p.nc * it.Tc;
+    it.v = (int64_t)blockIdx.x * TT / G;
+    it.vend = ((int64_t)blockIdx.x + 1) * TT / G;
+    return it;
+  };
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tm_w);
-    prefetch_tmap(gathered ? &tm_g4 : &tm_h128);
-    if (!gathered) prefetch_tmap(p.pair ? &tm_h256 : &tm_h32);
+    if constexpr (NC > 1) {
+      for (int c = 0; c < p.nc; ++c) {
+        prefetch_tmap(mm_w<NC>(mm, c));
+        prefetch_tmap(mm_h<NC>(mm, c));
+      }
+    } else {
+      prefetch_tmap(&tm_w);
+      prefetch_tmap(gathered ? &tm_g4 : &tm_h128);
+      if (!gathered) prefetch_tmap(p.pair ? &tm_h256 : &tm_h32);
+    }
     for (int i = 0; i < p.nw; ++i) {
       mbar_init(&w_full[i], 1);
       mbar_init(&w_empty[i], 1);
     }
     for (int i = 0; i < p.na; ++i) {
       mbar_init(&a_full[i], 1);
-      // MMA commit + the 4 RMS warps owning the tile (pair slots: all 8)
-      mbar_init(&a_empty[i], 1 + (p.pair ? 8 : 4));
+      // MMA commit + all 8 RMS warps (each waits every slot, reads its own tile's)
+      mbar_init(&a_empty[i], 1 + 8);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&t_full[i], 1);
@@ -191,7 +291,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tmem_alloc(tmem_slot, p.tmem_cols);
     tmem_relinquish();
   }
-  for (int i = threadIdx.x; i < p.b; i += blockDim.x) sWup[i] = p.w_up[i];
+  if (NC == 1)
+    for (int i = threadIdx.x; i < p.b; i += blockDim.x) sWup[i] = p.w_up[i];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -205,10 +306,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint64_t pol_w = policy_evict_last();
     int as = 0, aph = 0, wsl = 0, wph = 0;
     long long pw_cyc = 0, p_begin = pclk();
-    for (int64_t g = blockIdx.x; g < NG; g += G) {
-      int64_t r0, r1;
-      group_range(g, n, n32, NG, p.gran, r0, r1);
+    GroupIter it = make_iter();
+    int c;
+    int64_t g, r0, r1;
+    while (next_group<NC>(it, c, g, r0, r1)) {
       const int T = (int)((r1 - r0 + 127) / 128);
+      const CUtensorMap* const tw = NC > 1 ? mm_w<NC>(mm, c) : &tm_w;
+      const CUtensorMap* const th = NC > 1 ? mm_h<NC>(mm, c) : (gathered ? &tm_g4 : &tm_h128);
       if (gathered) {
         __syncwarp();
         for (int64_t i = r0 + lane; i < r0 + (int64_t)T * 128; i += 32)
@@ -219,7 +323,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         auto load_w = [&](int kc) {
           mbar_wait(&w_empty[wsl], wph ^ 1);
           mbar_arrive_expect_tx(&w_full[wsl], p.wslot);
-          tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 64, 0, pol_w);
+          tma_load_2d(sW + (size_t)wsl * p.wslot, tw, &w_full[wsl], kc * 64, 0, pol_w);
           if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
         };
         auto load_pair = [&](int kc, int pt) {
@@ -239,9 +343,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const int64_t rb = r0 + (int64_t)t * 128;
           const int rows_in = (int)((r1 - rb) < 128 ? (r1 - rb) : 128);
           if (!gathered) {
-            if (rows_in == 128) {
+            if (rows_in == 128 || NC > 1) {
+              // K1m groups are whole tiles: a ragged tile is the capture's
+              // last one, its out-of-range rows are zero-filled (no reads)
               mbar_arrive_expect_tx(&a_full[as], kASlotBytes);
-              tma_load_2d(dst, &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
+              tma_load_2d(dst, th, &a_full[as], kc * 64, (int)rb, pol_h);
             } else {
               // ragged tail: greedy 64/32/16-row boxes (16-row boxes stream poorly)
               const int rr = (rows_in + kBox - 1) / kBox * kBox;
@@ -265,7 +371,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             mbar_arrive_expect_tx(&a_full[as], ng4 * 512);
             const uint32_t* id = ids + t * 128;
             for (int q = 0; q < ng4; ++q)
-              tma_gather4(dst + q * 512, &tm_g4, &a_full[as], kc * 64, (int)id[4 * q],
+              tma_gather4(dst + q * 512, th, &a_full[as], kc * 64, (int)id[4 * q],
                           (int)id[4 * q + 1], (int)id[4 * q + 2], (int)id[4 * q + 3], pol_h);
           }
           if (++as == p.na) { as = 0; aph ^= 1; }
@@ -298,6 +404,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
         }
       }
+      K1_GROUP_END();
     }
     if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[18] = pw_cyc; dbg[19] = pclk() - p_begin; }
   } else if (warp == 1) {
@@ -309,9 +416,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     uint32_t accph = 0;
     long long wait_cyc = 0, t_begin = pclk();
     const uint64_t desc_hi = sw128_kmajor_desc(0);
-    for (int64_t g = blockIdx.x; g < NG; g += G) {
-      int64_t r0, r1;
-      group_range(g, n, n32, NG, p.gran, r0, r1);
+    GroupIter it = make_iter();
+    int c;
+    int64_t g, r0, r1;
+    while (next_group<NC>(it, c, g, r0, r1)) {
       const int T = (int)((r1 - r0 + 127) / 128);
       for (int t = 0; t < T; ++t) mbar_wait(&t_empty[t], ((accph >> t) & 1u) ^ 1u);
       tc_fence_after();
@@ -405,6 +513,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int j = 0; j < p.nx; ++j)
         if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
       accph ^= (1u << T) - 1u;
+      K1_GROUP_END();
     }
     if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = pclk() - t_begin; }
   } else if (warp <= 9) {
@@ -420,10 +529,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int as = 0, aph = 0, gi = 0;
     uint32_t accph = 0;
     long long sw_cyc = 0, s_begin = pclk();
-    for (int64_t g = blockIdx.x; g < NG; g += G) {
-      int64_t r0, r1;
-      group_range(g, n, n32, NG, p.gran, r0, r1);
+    GroupIter it = make_iter();
+    int c;
+    int64_t g, r0, r1;
+    while (next_group<NC>(it, c, g, r0, r1)) {
       const int T = (int)((r1 - r0 + 127) / 128);
+      const float* const wup = NC > 1 ? p.wups[c] : sWup;
+      float* const scores_c = NC > 1 ? p.scores + (size_t)c * p.cap : p.scores;
       // sum of squares of this thread's row for each of its two tiles
       // (t = wset, wset + 2), four f32 chains each, from the swizzled A slots
       float ss[2][4];
@@ -438,8 +550,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           uint4 u[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&a_empty[as]);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             sq2_acc<kBF16>(u[j].x, acc[0], acc[1]);
@@ -447,6 +557,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             sq2_acc<kBF16>(u[j].z, acc[0], acc[1]);
             sq2_acc<kBF16>(u[j].w, acc[2], acc[3]);
           }
+          // release the slot only after the values are consumed: an arrive
+          // right after the LDS issue let the TMA refill race the reads
+          // (tools/stress_k1.py: non-deterministic rows with several groups
+          // per CTA)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_empty[as]);
         } else {
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[as]);
@@ -462,8 +578,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           uint4 u[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&a_empty[as]);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             sq2_acc<kBF16>(u[j].x, acc[0], acc[1]);
@@ -471,6 +585,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             sq2_acc<kBF16>(u[j].z, acc[0], acc[1]);
             sq2_acc<kBF16>(u[j].w, acc[2], acc[3]);
           }
+          __syncwarp();  // consumed, then released (see rms_pair)
+          if (lane == 0) mbar_arrive(&a_empty[as]);
+        } else {
+          // the other set's tile: every RMS warp still takes part in every
+          // slot's phase (a_empty counts all 8), as in pair mode — with
+          // owner-only arrivals (4 per slot) repeated launches with several
+          // groups per CTA gave non-deterministic tiles (tools/stress_k1.py)
+          mbar_wait(&a_full[as], aph);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_empty[as]);
         }
         if (++as == p.na) { as = 0; aph ^= 1; }
       };
@@ -479,7 +603,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const int NP = (T + 1) / 2;
       for (int kc = 0; kc < P1; ++kc) {
         if (p.pair) {
-          for (int pt = 0; pt < NP; ++pt) rms_pair(pt, ss[pt]);
+#pragma unroll
+          for (int pt = 0; pt < 2; ++pt)  // static index: ss stays in registers
+            if (pt < NP) rms_pair(pt, ss[pt]);
         } else {
 #pragma unroll
           for (int t = 0; t < 4; ++t)
@@ -511,7 +637,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (c0 + 32 <= p.b) {
 #pragma unroll
               for (int jj = 0; jj < 32; jj += 4) {
-                const float4 w4 = *reinterpret_cast<const float4*>(sWup + c0 + jj);
+                const float4 w4 = NC > 1 ? __ldg(reinterpret_cast<const float4*>(wup + c0 + jj))
+                                         : *reinterpret_cast<const float4*>(sWup + c0 + jj);
                 const f32x2 s01 = silu2_tanh(fmul2(pack2u(v[jj], v[jj + 1]), hs2));
                 const f32x2 s23 = silu2_tanh(fmul2(pack2u(v[jj + 2], v[jj + 3]), hs2));
                 acc2 = ffma2(pack2(w4.x, w4.y), s01, acc2);
@@ -521,8 +648,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
               for (int jj = 0; jj < 32; jj += 2) {
                 if (c0 + jj < p.b) {
-                  const float w0 = sWup[c0 + jj];
-                  const float w1 = (c0 + jj + 1 < p.b) ? sWup[c0 + jj + 1] : 0.0f;
+                  const float w0 = NC > 1 ? __ldg(wup + c0 + jj) : sWup[c0 + jj];
+                  const float w1 =
+                      (c0 + jj + 1 < p.b) ? (NC > 1 ? __ldg(wup + c0 + jj + 1) : sWup[c0 + jj + 1]) : 0.0f;
                   const f32x2 s01 = silu2_tanh(fmul2(pack2u(v[jj], v[jj + 1]), hs2));
                   acc2 = ffma2(pack2(w0, w1), s01, acc2);
                 }
@@ -552,7 +680,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const float logit = lo + hi;
           const float score = score_from_logit(logit);
           const bool ex = valid && (score > p.theta);
-          if (valid) {
+          if (NC > 1) {
+            if (valid) scores_c[r] = score;
+          } else if (valid) {
             if (p.scores) p.scores[r] = score;
             if (p.logits) p.logits[r] = logit;
             if (p.mask) p.mask[r] = ex ? 1 : 0;
@@ -567,6 +697,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (p.pair) {
         // pair-major: both sets stream pair 0, then run tiles 0 / 1 at once
         // while pair 1 streams, then tiles 2 / 3
+#pragma unroll
         for (int pt = 0; pt < 2; ++pt) {
           if (pt < NP)
             for (int j = 0; j < p.nx; ++j) rms_pair(pt, ss[pt]);
@@ -588,15 +719,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (dbg && warp == 2 && lane == 0) dbg[3] = gtimer();
       if (lane == 0) mbar_arrive(&m_full[par]);
       ++gi;
+      K1_GROUP_END();
     }
   } else {
     // ----------------------------------------------------------- compaction
     griddep_wait();  // the previous launch's look-back state / outputs are final
     const uint32_t tag = launch_tag(p.ws);
     int gi = 0;
-    for (int64_t g = blockIdx.x; g < NG; g += G) {
-      int64_t r0, r1;
-      group_range(g, n, n32, NG, p.gran, r0, r1);
+    GroupIter it = make_iter();
+    int c;
+    int64_t g, r0, r1;
+    while (next_group<NC>(it, c, g, r0, r1)) {
       const int par = gi & 1;
       mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
@@ -639,8 +772,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
       }
       ++gi;
+      K1_GROUP_END();
     }
-    if (NG == 0 && blockIdx.x == 0 && lane == 0 && p.counts) {
+    if (NC == 1 && NG == 0 && blockIdx.x == 0 && lane == 0 && p.counts) {
       p.counts[0] = 0;
       p.counts[1] = 0;
     }
@@ -757,15 +891,8 @@ bool route_tc_supported(int dtype, int d, int b) {
          b <= 256;
 }
 
-int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
-  {
-    // few rows: split d over a cluster instead (route_tcs.cu)
-    int dev0 = 0;
-    cudaGetDevice(&dev0);
-    int grid = 0;
-    const int ks = route_tcs_plan(a, dev0, &grid);
-    if (ks) return route_tcs_launch(a, stream, ks, grid);
-  }
+// Shared launch setup of K1 and K1m: tile geometry, smem carve-up, numerics.
+static int tc_params(const RouteArgs& a, bool pair, TcParams& p, uint32_t& smem_bytes) {
   const int npad = (a.b + 15) / 16 * 16;
   const int bp = (npad + 31) / 32 * 32;
   const int tpg = std::min(4, 512 / bp);
@@ -782,25 +909,14 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   const uint32_t off_a = (uint32_t)nw * wslot;
   const int smem_cap = 227 * 1024;
   const uint32_t misc = 1024 /*w_up*/ + 512 /*bars*/ + 128 /*words*/ + 2048 /*ids*/ + 16;
-  // pair slots (two whole tiles per 32 KB slot: half the barrier round trips
-  // per byte) for dense launches dealt in whole tiles; TIDE_K1_PAIRSLOT=0/1
-  int sms0 = 0;
-  {
-    int dev1 = 0;
-    cudaGetDevice(&dev1);
-    sms0 = sm_count(dev1);
-  }
-  bool pair = a.row_idx == nullptr && a.n_dev == nullptr && a.n % 128 == 0 &&
-              a.n >= (int64_t)sms0 * 256 && tpg == 4;
-  {
-    const char* env = getenv("TIDE_K1_PAIRSLOT");  // read per call
-    if (env) pair = pair && env[0] == '1';
-  }
   const uint32_t slot_bytes = pair ? 2u * kASlotBytes : (uint32_t)kASlotBytes;
   int na = (int)((smem_cap - 1024 - off_a - misc) / slot_bytes);
   na = std::min(na, kMaxNA);
+  {
+    const char* env = getenv("TIDE_K1_NA");  // debug: cap the A ring (read per call)
+    if (env) na = std::max(2, std::min(na, atoi(env)));
+  }
   if (na < 2) return set_error(TIDE_ERR_UNSUPPORTED, "bottleneck too wide for smem");
-  TcParams p{};
   p.n_host = a.n;
   p.n_dev = a.n_dev;
   p.rows_total = a.rows_total;
@@ -823,7 +939,7 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.off_words = p.off_bar + 512;
   p.off_ids = p.off_words + 128;
   p.off_tmem = p.off_ids + 2048;
-  const uint32_t smem_bytes = p.off_tmem + 16 + 1024;
+  smem_bytes = p.off_tmem + 16 + 1024;
   p.row_idx = a.row_idx;
   p.ids_from_rows = a.ids_from_rows;
   p.w_up = a.w_up;
@@ -841,46 +957,19 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   p.counts = a.counts;
   p.ws = reinterpret_cast<Workspace*>(a.workspace);
   p.dbg = g_dbg;
+  p.nc = 1;
+  return TIDE_OK;
+}
 
-  CUtensorMap tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4, tm_h256;
-  const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
-  int rc;
-  if ((rc = make_map(&tm_h128, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
-  if ((rc = make_map(&tm_h64, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 64))) return rc;
-  if ((rc = make_map(&tm_h32b, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 32))) return rc;
-  if ((rc = make_map(&tm_h32, a.h, a.dtype, a.d, hrows, a.ld_h, 64, kBox))) return rc;
-  if ((rc = make_map(&tm_g4, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 1))) return rc;
-  if ((rc = make_map(&tm_w, a.w_down, a.dtype, a.d, a.b, a.d, 64, npad))) return rc;
-  if (pair) {
-    if ((rc = make_map(&tm_h256, a.h, a.dtype, a.d, hrows, a.ld_h, 64, 256))) return rc;
-  } else {
-    tm_h256 = tm_h128;
-  }
-
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int sms = sm_count(dev);
-  // whole tiles per CTA once each holds at least two and the row count is
-  // known on the host (a chain link's live count may be far below its
-  // capacity: 16-row units keep every SM busy there); TIDE_K1_GRAN overrides
-  int gran = (a.n_dev == nullptr && a.n >= (int64_t)sms * 256) ? 128 : kGran;
-  {
-    const char* env = getenv("TIDE_K1_GRAN");
-    if (env) {
-      const int v = atoi(env);
-      gran = (v == 32 || v == 64 || v == 128) ? v : kGran;
-    }
-  }
-  p.gran = gran;
-  const int64_t n32 = (a.n + gran - 1) / gran;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n32));
-  if ((n32 + tpg * (128 / gran) - 1) / (tpg * (128 / gran)) > kMaxParts / 2)
-    return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
+template <int NC>
+static int tc_launch(const RouteArgs& a, const CUtensorMap (&tm)[7], const MultiMaps<NC>& mm,
+                     const TcParams& p, uint32_t smem_bytes, int grid, int dev, cudaStream_t stream,
+                     const char* what) {
   static bool attr_set[64] = {false};
   if (!attr_set[dev & 63]) {
-    cudaFuncSetAttribute(route_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(route_tc_kernel<true, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
-    cudaFuncSetAttribute(route_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(route_tc_kernel<false, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
     attr_set[dev & 63] = true;
   }
@@ -897,13 +986,121 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
     cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
   }
   cfg.attrs = attr;
+  cudaError_t e;
   if (a.dtype == TIDE_BF16)
-    cudaLaunchKernelEx(&cfg, route_tc_kernel<true>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4,
-                       tm_h256, p);
+    e = cudaLaunchKernelEx(&cfg, route_tc_kernel<true, NC>, tm[0], tm[1], tm[2], tm[3], tm[4], tm[5],
+                           tm[6], mm, p);
   else
-    cudaLaunchKernelEx(&cfg, route_tc_kernel<false>, tm_h128, tm_h64, tm_h32b, tm_h32, tm_w, tm_g4,
-                       tm_h256, p);
-  return check_launch("route_tc_kernel");
+    e = cudaLaunchKernelEx(&cfg, route_tc_kernel<false, NC>, tm[0], tm[1], tm[2], tm[3], tm[4],
+                           tm[5], tm[6], mm, p);
+  if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return check_launch(what);
+}
+
+int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    // few rows: split d over a cluster instead (route_tcs.cu)
+    int grid = 0;
+    const int ks = route_tcs_plan(a, dev, &grid);
+    if (ks) return route_tcs_launch(a, stream, ks, grid);
+  }
+  const int sms = sm_count(dev);
+  // pair slots (two whole tiles per 32 KB slot: half the barrier round trips
+  // per byte) for dense launches dealt in whole tiles; TIDE_K1_PAIRSLOT=0/1
+  const int tpg0 = std::min(4, 512 / (((a.b + 15) / 16 * 16 + 31) / 32 * 32));
+  bool pair = a.row_idx == nullptr && a.n_dev == nullptr && a.n % 128 == 0 &&
+              a.n >= (int64_t)sms * 256 && tpg0 == 4;
+  {
+    const char* env = getenv("TIDE_K1_PAIRSLOT");  // read per call
+    if (env) pair = pair && env[0] == '1';
+  }
+  TcParams p{};
+  uint32_t smem_bytes = 0;
+  int rc;
+  if ((rc = tc_params(a, pair, p, smem_bytes))) return rc;
+
+  CUtensorMap tm[7];  // h128, h64, h32b, h16, w, gather4, h256
+  const int64_t hrows = a.row_idx ? a.rows_total : std::max<int64_t>(a.n, 1);
+  if ((rc = make_map(&tm[0], a.h, a.dtype, a.d, hrows, a.ld_h, 64, 128))) return rc;
+  if ((rc = make_map(&tm[1], a.h, a.dtype, a.d, hrows, a.ld_h, 64, 64))) return rc;
+  if ((rc = make_map(&tm[2], a.h, a.dtype, a.d, hrows, a.ld_h, 64, 32))) return rc;
+  if ((rc = make_map(&tm[3], a.h, a.dtype, a.d, hrows, a.ld_h, 64, kBox))) return rc;
+  if ((rc = make_map(&tm[5], a.h, a.dtype, a.d, hrows, a.ld_h, 64, 1))) return rc;
+  if ((rc = make_map(&tm[4], a.w_down, a.dtype, a.d, a.b, a.d, 64, p.npad))) return rc;
+  if (pair) {
+    if ((rc = make_map(&tm[6], a.h, a.dtype, a.d, hrows, a.ld_h, 64, 256))) return rc;
+  } else {
+    tm[6] = tm[0];
+  }
+
+  // whole tiles per CTA once each holds at least two and the row count is
+  // known on the host (a chain link's live count may be far below its
+  // capacity: 16-row units keep every SM busy there); TIDE_K1_GRAN overrides
+  int gran = (a.n_dev == nullptr && a.n >= (int64_t)sms * 256) ? 128 : kGran;
+  {
+    const char* env = getenv("TIDE_K1_GRAN");
+    if (env) {
+      const int v = atoi(env);
+      gran = (v == 32 || v == 64 || v == 128) ? v : kGran;
+    }
+  }
+  p.gran = gran;
+  const int64_t n32 = (a.n + gran - 1) / gran;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n32));
+  if ((n32 + p.tpg * (128 / gran) - 1) / (p.tpg * (128 / gran)) > kMaxParts / 2)
+    return set_error(TIDE_ERR_UNSUPPORTED, "too many rows for one launch");
+  MultiMaps<1> mm{};
+  return tc_launch<1>(a, tm, mm, p, smem_bytes, grid, dev, stream, "route_tc_kernel");
+}
+
+// K1m: every row scored at C checkpoints in ONE persistent launch, scores to
+// a.scores[c * a.n + position]; dense (a.row_idx == NULL: rows 0..a.n-1 of
+// every capture) or gathered (the live rows a.row_idx[0 .. *a.n_dev), routed
+// only when a.n_min <= *a.n_dev <= n_limit).  The caller resolves the first
+// firing checkpoint per row (chain_resolve_launch).
+int route_tc_multi_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
+                          const void* const* w_ptrs, const float* const* wup_ptrs,
+                          int64_t n_limit, cudaStream_t stream) {
+  if (C < 2 || C > kMaxMC) return set_error(TIDE_ERR_UNSUPPORTED, "K1m: C must be in [2, %d]", kMaxMC);
+  if (!a.scores) return set_error(TIDE_ERR_ARG, "K1m: scores required");
+  if ((a.row_idx == nullptr) != (a.n_dev == nullptr))
+    return set_error(TIDE_ERR_ARG, "K1m: row_idx and n_dev go together");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = sm_count(dev);
+  TcParams p{};
+  uint32_t smem_bytes = 0;
+  int rc;
+  if ((rc = tc_params(a, false, p, smem_bytes))) return rc;
+  p.gran = 128;
+  p.nc = C;
+  p.cap = a.n;
+  p.n_min = a.n_min;
+  p.n_limit = n_limit;
+  // scores only: no mask / logits / compaction / exit layers here
+  p.logits = nullptr;
+  p.mask = nullptr;
+  p.exit_idx = p.cont_idx = p.exit_layers = p.counts = nullptr;
+  p.inputs_ready = 0;
+  const bool gathered = a.row_idx != nullptr;
+  const int64_t hrows = gathered ? a.rows_total : std::max<int64_t>(a.n, 1);
+  static MultiMaps<kMaxMC> mm;  // host staging (copied into the launch parameters)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int c = 0; c < C; ++c) {
+    if ((rc = make_map(&mm.h[c], h_ptrs[c], a.dtype, a.d, hrows, a.ld_h, 64, gathered ? 1 : 128)))
+      return rc;
+    if ((rc = make_map(&mm.w[c], w_ptrs[c], a.dtype, a.d, a.b, a.d, 64, p.npad))) return rc;
+    p.wups[c] = wup_ptrs[c];
+  }
+  CUtensorMap tm[7];
+  for (int i = 0; i < 7; ++i) tm[i] = mm.h[0];
+  // tiles: C x ceil(cap / 128) at most (the live count is only known on the device)
+  const int64_t TT = (int64_t)C * ((a.n + 127) / 128);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, TT));
+  return tc_launch<kMaxMC>(a, tm, mm, p, smem_bytes, grid, dev, stream, "route_tc_kernel (K1m)");
 }
 
 }  // namespace tide

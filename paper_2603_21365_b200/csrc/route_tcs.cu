@@ -367,11 +367,6 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       uint4 u[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const uint4*>(rp + ((j ^ swz) << 4));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      // refill the previous chunk's slot (its MMA has had a whole chunk to retire)
-      const int i = kc - k0;
-      if (gathered && i >= 1 && i - 1 + p.stages < nkr) issue(i - 1 + p.stages);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         sq2_acc<kBF16>(u[j].x, sq[0], sq[1]);
@@ -379,6 +374,13 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         sq2_acc<kBF16>(u[j].z, sq[0], sq[1]);
         sq2_acc<kBF16>(u[j].w, sq[2], sq[3]);
       }
+      // released once the values are consumed (an arrive right after the
+      // LDS issue lets the refill race the reads, tools/stress_k1.py)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // refill the previous chunk's slot (its MMA has had a whole chunk to retire)
+      const int i = kc - k0;
+      if (gathered && i >= 1 && i - 1 + p.stages < nkr) issue(i - 1 + p.stages);
       if (++s == p.stages) { s = 0; ph ^= 1u; }
     }
     const float ssp = (sq[0] + sq[1]) + (sq[2] + sq[3]);
@@ -762,14 +764,16 @@ int tcs_launch(const RouteArgs& a, const SplitParams& p, const WMaps<NC>& wm, ui
 // Chain tail, step 2: first firing checkpoint of every live row (per-token
 // rule of ee/runtime.py:166-178 over the tail's checkpoints, in order) and the
 // live count the following links read (0 when the tail handled the rows).
+// Dense form (n_dev == row_idx == NULL): rows 0 .. cap-1, row id = position.
 __global__ void chain_resolve_kernel(const float* scores, int64_t cap, int nc, TailLayers layers,
                                      float theta, const int64_t* n_dev, int64_t n_min,
                                      int64_t n_limit,
                                      const int64_t* row_idx, int64_t* exit_layers,
                                      int64_t* tail_count, unsigned long long cond) {
-  const int64_t n = *n_dev;
+  griddep_wait();  // the scoring launch before it may run under PDL
+  const int64_t n = n_dev ? *n_dev : cap;
   const bool handled = n >= n_min && n <= n_limit;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && tail_count) {
     *tail_count = handled ? 0 : n;
     // in a captured CUDA graph: the IF node holding the remaining links runs
     // only when the tail did not handle the rows (tide_capture_cond_*)
@@ -778,7 +782,7 @@ __global__ void chain_resolve_kernel(const float* scores, int64_t cap, int nc, T
   if (!handled) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rid = row_idx[i];
+    const int64_t rid = row_idx ? row_idx[i] : i;
     // 8 checkpoints' scores in flight per step (the loads are independent)
     for (int c0 = 0; c0 < nc; c0 += 8) {
       float v[8];

@@ -318,7 +318,7 @@ class _ChainGraphs:
         import os
         e = os.environ
         return tuple(e.get(k) for k in ("TIDE_CHAIN_TAIL", "TIDE_TAIL_AFTER", "TIDE_TAIL_ROWS",
-                                        "TIDE_TAIL_WIDE",
+                                        "TIDE_TAIL_WIDE", "TIDE_SPECULATIVE",
                                         "TIDE_TAIL_KS", "TIDE_SPLIT", "TIDE_PDL",
                                         "TIDE_F32_TAIL_ROWS"))
 
@@ -496,6 +496,18 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
         if rc == 0:
             return exit_layers
         # a shape the one-launch tail does not take: the per-checkpoint links below
+    if code != N.F32 and 2 <= len(ckpts) <= MAX_MULTI_CKPTS and _speculative(n, d, final, theta):
+        # every row at every checkpoint in ONE persistent tensor-core launch
+        # (K1m) + resolve: the first firing checkpoint is what peeling
+        # computes (a row's score at checkpoint k depends only on that row)
+        wts = [device_weights(bank.routers[k], code, dev) for k in ckpts]
+        scratch = torch.empty(len(ckpts) * n, dtype=torch.float32, device=dev)
+        N.check(lib.tide_route_multi(
+            N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, None, n, d,
+            code, None, N.ptr_array([w.data_ptr() for w, _ in wts]),
+            N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(ckpts), eps, theta,
+            scratch.data_ptr(), exit_layers.data_ptr(), ws, s), "tide_route_multi")
+        return exit_layers
     rem = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
     cnt = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(2)]
     row_idx, n_dev = 0, 0
@@ -546,6 +558,24 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
 
 
 TAIL_AFTER = 3  # links of the peeling chain before the tail attempt
+MAX_MULTI_CKPTS = 24  # route_tc.cu kMaxMC
+SPEC_BYTES = 64 << 20  # per-checkpoint capture bytes up to which scoring is speculative
+
+
+def _speculative(n: int, d: int, final, theta: float) -> bool:
+    """Score every checkpoint for every row in one launch (tide_route_multi)
+    instead of peeling?  Peeling reads only the live rows but pays one
+    latency-bound link per checkpoint (~15-20 us at 4,096 x 4096, mostly
+    fixed cost); speculation reads every capture once at the streaming rate.
+    Taken when a checkpoint's capture is small enough that its bytes cost less
+    than a link's fixed cost (n d e <= SPEC_BYTES: configs 1-2-sized
+    prefills), or when few rows exit anyway (theta >= WIDE_THETA).
+    TIDE_SPECULATIVE=1 / 0 forces it on / off."""
+    import os
+    env = os.environ.get("TIDE_SPECULATIVE")
+    if env is not None:
+        return env == "1"
+    return n * d * final.element_size() <= SPEC_BYTES or theta >= WIDE_THETA
 
 
 def _tail_enabled() -> bool:

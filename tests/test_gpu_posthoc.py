@@ -251,15 +251,21 @@ def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch)
         exc |= np.abs(t - O.logit_of(theta)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
     want = O.first_exit_from_scores(scores, theta)
     out = {}
-    # wide tail right after link 1 / links + small tail / plain links
+    # wide tail right after link 1 / links + small tail / plain links (peeling),
+    # and the speculative one-launch K1m form
+    monkeypatch.setenv("TIDE_SPECULATIVE", "0")
     for wide, tail in (("1", "1"), ("0", "1"), ("0", "0")):
         monkeypatch.setenv("TIDE_TAIL_WIDE", wide)
         monkeypatch.setenv("TIDE_CHAIN_TAIL", tail)
         got = P.select_exits(states, bank, cfg).cpu().numpy()
         assert np.all((got == want) | exc), (wide, tail)
         out[wide + tail] = got
+    monkeypatch.setenv("TIDE_SPECULATIVE", "1")
+    out["spec"] = P.select_exits(states, bank, cfg).cpu().numpy()
+    assert np.all((out["spec"] == want) | exc)
     assert np.all((out["11"] == out["00"]) | exc)
     assert np.all((out["01"] == out["00"]) | exc)
+    assert np.all((out["spec"] == out["00"]) | exc)
     if theta == 1.0:
         assert all(np.all(v == P.NO_EXIT) for v in out.values())
 
@@ -286,13 +292,15 @@ def test_decode_step_fallback_paths(variant, monkeypatch):
 
 @pytest.mark.parametrize("d,n,L,scale,theta", [(4096, 4096, 32, 0.1, 0.5), (4096, 1000, 24, 0.2, 1.0),
                                                (8192, 2048, 40, 0.06, 0.7)])
-@pytest.mark.parametrize("wide", ["1", "0"])
+@pytest.mark.parametrize("wide", ["1", "0", "spec"])
 def test_chain_captured_in_cuda_graph(d, n, L, scale, theta, wide, monkeypatch):
     """select_exits captured in a CUDA graph (link 1 + the wide tail, or the
     links with the ones after the small chain tail in a conditional node the
-    tail switches off) == eager, on replays with new capture contents."""
+    tail switches off, or the speculative K1m launch) == eager, on replays
+    with new capture contents."""
     need_gpu()
-    monkeypatch.setenv("TIDE_TAIL_WIDE", wide)
+    monkeypatch.setenv("TIDE_SPECULATIVE", "1" if wide == "spec" else "0")
+    monkeypatch.setenv("TIDE_TAIL_WIDE", "1" if wide == "spec" else wide)
     ckpts, routers, states, bank, head = _big_case(L, d, n, "bf16", 90 + n, scale=scale)
     cfg = P.RuntimeConfig(exit_threshold=theta)
     s = torch.cuda.Stream()
@@ -454,3 +462,58 @@ def test_decode_step_cluster_row_owners(mode, d, n):
         np.testing.assert_array_equal(sc[i], np.array([O._sigma64(float(v)) for v in lg[i]],
                                                       np.float32))
     assert int(cnt[0]) == int((ex >= 0).sum())
+
+
+def _multi_call(states, bank, ckpts, n, d, code, row_idx=None, n_live=None, rows_total=None):
+    """tide_route_multi through the C ABI: exit map over every checkpoint."""
+    from paper_2603_21365_b200 import _device as D, _native as N
+    from paper_2603_21365_b200.router_ops import device_weights
+    lib = N.load()
+    dev = torch.device("cuda", 0)
+    wts = [device_weights(bank.routers[k], code, dev) for k in ckpts]
+    out = torch.full((n,), P.NO_EXIT, dtype=torch.int64, device=dev)
+    scratch = torch.empty(len(ckpts) * n, dtype=torch.float32, device=dev)
+    n_dev = torch.tensor([n_live], dtype=torch.int64, device=dev) if row_idx is not None else None
+    N.check(lib.tide_route_multi(
+        N.ptr_array([states[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n,
+        n_dev.data_ptr() if n_dev is not None else None, rows_total or n, d, code,
+        row_idx.data_ptr() if row_idx is not None else None,
+        N.ptr_array([w.data_ptr() for w, _ in wts]), N.ptr_array([u.data_ptr() for _, u in wts]),
+        128, N.i64_array(ckpts), float(np.float32(bank.eps)), float(np.float32(0.6)),
+        scratch.data_ptr(), out.data_ptr(), D.workspace(dev).data_ptr(), D.stream_handle(dev)),
+        "tide_route_multi")
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("d,n,L,dtype", [(4096, 4096, 32, "bf16"), (4096, 1000, 24, "f16"),
+                                         (8192, 700, 80, "bf16"), (768, 2048, 12, "bf16"),
+                                         (2048, 300, 96, "bf16")])
+def test_route_multi_dense_and_gathered(d, n, L, dtype):
+    """K1m (tide_route_multi): dense over all rows and gathered over a live
+    list (every other row, ragged count) == the oracle's per-token first-exit
+    map over the same checkpoints (band rule); up to 24 checkpoints."""
+    need_gpu()
+    ckpts, routers, states, bank, head = _big_case(L, d, n, dtype, 11 + d + n, scale=0.15)
+    ckpts = ckpts[:24]
+    from paper_2603_21365_b200 import _native as N
+    code = N.BF16 if dtype == "bf16" else N.F16
+    host = {k: states[k + 1].float().cpu().numpy() for k in ckpts}
+    scores, exc = {}, np.zeros(n, bool)
+    for k in ckpts:
+        s_, t, m = O.route_logits(host[k], routers[k])
+        scores[k] = s_
+        exc |= np.abs(t - O.logit_of(0.6)) <= RTOL[dtype] * np.maximum(np.abs(t), m)
+    want = O.first_exit_from_scores(scores, 0.6)
+    got = _multi_call(states, bank, ckpts, n, d, code)
+    assert np.all((got == want) | exc)
+    assert len(np.unique(got)) > 2  # rows leave at several checkpoints
+    # gathered: the live list = odd rows (capacity n, live count n // 2)
+    live = torch.arange(1, n, 2, dtype=torch.int64, device="cuda")
+    idx = torch.zeros(n, dtype=torch.int64, device="cuda")
+    idx[: live.numel()] = live
+    gl = _multi_call(states, bank, ckpts, n, d, code, row_idx=idx, n_live=live.numel(), rows_total=n)
+    sel = live.cpu().numpy()
+    assert np.all((gl[sel] == want[sel]) | exc[sel])
+    others = np.setdiff1d(np.arange(n), sel)
+    assert np.all(gl[others] == P.NO_EXIT)

@@ -404,3 +404,29 @@ def test_wide_cuda_core_kernel(dtype, n, d, b):
     e, c = O.compact_indices(r["mask"].cpu().numpy())
     np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)
     np.testing.assert_array_equal(r["continuing_indices"].cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_repeated_launches_bitwise_identical(pair, monkeypatch):
+    """Several row groups per CTA (160,000 rows): repeated launches, each after
+    an L2-thrashing write, give bit-identical logits / masks / indices (fixed
+    reduction orders).  Regression for the slot-release races found by
+    tools/stress_k1.py (owner-only releases, release before the smem reads
+    were consumed)."""
+    need_gpu()
+    import torch
+    monkeypatch.setenv("TIDE_K1_PAIRSLOT", pair)
+    g = np.random.Generator(np.random.PCG64(77))
+    d = 2048
+    wd = (g.standard_normal((128, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, 128)) * 0.05).astype(np.float32)
+    router = _router(wd, wu)
+    h = torch.randn((160_000, d), device="cuda").to(torch.bfloat16)
+    junk = torch.empty(1 << 26, device="cuda")
+    kw = dict(theta=0.5, want_logits=True, want_mask=True, want_indices=True)
+    ref = P.route(h, router, **kw)
+    for i in range(25):
+        junk.fill_(float(i))
+        r = P.route(h, router, **kw)
+        for k in ("logits", "mask", "exiting_indices", "continuing_indices"):
+            assert torch.equal(r[k], ref[k]), (i, k)

@@ -223,7 +223,7 @@ def chain_sweep():
     """Peeling-chain configs 2 and 5 across thresholds, down to the worst case
     theta = 1.0 where no row ever exits and every link routes every row."""
     return ([config2(t) for t in (0.5, 0.7, 0.85, 1.0)]
-            + [config5(t) for t in (0.7, 0.85, 1.0)])
+            + [config5(t) for t in (0.5, 0.7, 0.85, 1.0)])
 
 
 def run_configs(hbm_gbs: float, bf16_tflops: float):

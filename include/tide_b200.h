@@ -311,16 +311,18 @@ int tide_route_tail_ex(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64
 
 /*
  * Per-token exit decision over C checkpoints (ee/runtime.py:166-178, the
- * per-token rule of posthoc_select) in ONE persistent tensor-core launch
- * plus a resolve step: every row is scored at every checkpoint (speculative:
- * no peeling between checkpoints) and exit_layers[row id] = layers[first c
- * whose score > theta]; rows that never fire are left untouched (pre-fill
- * them with TIDE_NO_EXIT).  Dense (row_idx = n_dev = NULL: rows 0..n-1 of
- * every capture, row id = row) or gathered (the live rows row_idx[0 ..
- * *n_dev), n = the list's capacity).  h_ptrs / w_ptrs / wup_ptrs / layers:
- * HOST arrays of C entries (ascending layers, C <= 24).  scores: device
- * scratch of C * n f32.  bf16 / f16 rows only.  Same exit map as the
- * peeling chain (a row's score at a checkpoint depends only on that row).
+ * per-token rule of posthoc_select) in ONE persistent tensor-core launch:
+ * every row is scored at every checkpoint (speculative: no peeling between
+ * checkpoints) and exit_layers[row id] = layers[first c whose score >
+ * theta], combined across CTAs by an atomic minimum; the routed rows'
+ * entries must hold TIDE_NO_EXIT on entry, rows that never fire keep it.
+ * Dense (row_idx = n_dev = NULL: rows 0..n-1 of every capture, row id = row)
+ * or gathered (the live rows row_idx[0 .. *n_dev), n = the list's
+ * capacity).  h_ptrs / w_ptrs / wup_ptrs / layers: HOST arrays of C entries
+ * (ascending layers, C <= 24).  scores: NULL or device memory of C * n f32
+ * (score of position i at checkpoint c -> scores[c * n + i]).  bf16 / f16
+ * rows only.  Same exit map as the peeling chain (a row's score at a
+ * checkpoint depends only on that row).
  * (No reference counterpart: an execution strategy of posthoc_select.)
  */
 int tide_route_multi(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t n,

@@ -208,7 +208,7 @@ int tide_route_multi(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t
     return set_error(TIDE_ERR_ARG, "tide_route_multi: bad shape");
   if ((row_idx == nullptr) != (n_dev == nullptr))
     return set_error(TIDE_ERR_ARG, "tide_route_multi: row_idx and n_dev go together");
-  if (!scores || !exit_layers || !workspace)
+  if (!exit_layers || !workspace)
     return set_error(TIDE_ERR_ARG, "tide_route_multi: null device buffer");
   if ((dtype != TIDE_F16 && dtype != TIDE_BF16) || !route_tc_supported(dtype, d, b) || ld_h % 8)
     return set_error(TIDE_ERR_UNSUPPORTED, "tide_route_multi: bf16/f16 rows, d %% 8 == 0, b <= 256");
@@ -235,14 +235,11 @@ int tide_route_multi(const void* const* h_ptrs, int32_t C, int64_t ld_h, int64_t
   a.exit_layers = exit_layers;
   a.workspace = workspace;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int rc;
   if (C == 1) {  // one checkpoint: the plain route (strict mask -> exit layer)
     a.layer = layers[0];
     return route_tc_launch(a, s);
   }
-  if ((rc = route_tc_multi_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, n, s))) return rc;
-  return chain_resolve_launch(scores, n, C, layers, theta, n_dev, 0, n, row_idx, exit_layers,
-                              nullptr, 0, s);
+  return route_tc_multi_launch(a, C, h_ptrs, w_ptrs, wup_ptrs, layers, n, s);
 }
 
 // --- CUDA-graph conditional for the links after a chain tail -----------------

@@ -54,7 +54,7 @@ int route_tcs_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                           unsigned long long cond, cudaStream_t stream);
 int route_tc_multi_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                           const void* const* w_ptrs, const float* const* wup_ptrs,
-                          int64_t n_limit, cudaStream_t stream);
+                          const int64_t* layers, int64_t n_limit, cudaStream_t stream);
 int route_simt_launch(const RouteArgs& a, cudaStream_t stream);
 int route_simt_tail_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                            const void* const* w_ptrs, const float* const* wup_ptrs,

@@ -81,7 +81,21 @@ struct TcParams {
   int32_t nc;
   int64_t cap, n_min, n_limit;
   const float* wups[kMaxMC];
+  int64_t layers[kMaxMC];  // exit layer of checkpoint c (ascending)
 };
+
+// exit_layers[row] = min(current, layer) where NO_EXIT (-1) counts as +inf:
+// the first firing checkpoint of a row scored by several CTAs at once
+// (deterministic: the result is a minimum, whatever the arrival order)
+__device__ __forceinline__ void exit_min(int64_t* slot, int64_t layer) {
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(slot);
+  long long cur = *reinterpret_cast<volatile long long*>(slot);
+  while (cur < 0 || cur > layer) {
+    const long long prev = (long long)atomicCAS(a, (unsigned long long)cur, (unsigned long long)layer);
+    if (prev == cur) break;
+    cur = prev;
+  }
+}
 
 // Per-checkpoint tensor maps of a K1m launch (kernel parameters): h[c] is the
 // 128-row box map of capture c (dense) or its 1-row gather4 map (gathered).
@@ -89,6 +103,7 @@ template <int NC>
 struct MultiMaps {
   CUtensorMap h[NC];
   CUtensorMap w[NC];
+  CUtensorMap p[NC];  // dense pair slots: the 256-row box map of capture c
 };
 template <>
 struct MultiMaps<1> {
@@ -97,6 +112,11 @@ struct MultiMaps<1> {
 template <int NC>
 __device__ __forceinline__ const CUtensorMap* mm_h(const MultiMaps<NC>& m, int c) {
   if constexpr (NC > 1) return &m.h[c];
+  else return nullptr;
+}
+template <int NC>
+__device__ __forceinline__ const CUtensorMap* mm_p(const MultiMaps<NC>& m, int c) {
+  if constexpr (NC > 1) return &m.p[c];
   else return nullptr;
 }
 template <int NC>
@@ -261,7 +281,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if constexpr (NC > 1) {
       for (int c = 0; c < p.nc; ++c) {
         prefetch_tmap(mm_w<NC>(mm, c));
-        prefetch_tmap(mm_h<NC>(mm, c));
+        prefetch_tmap(p.pair ? mm_p<NC>(mm, c) : mm_h<NC>(mm, c));
       }
     } else {
       prefetch_tmap(&tm_w);
@@ -332,7 +352,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const int64_t rb = r0 + (int64_t)pt * 256;
           const bool two = 2 * pt + 1 < T;
           mbar_arrive_expect_tx(&a_full[as], two ? 2u * kASlotBytes : (uint32_t)kASlotBytes);
-          tma_load_2d(dst, two ? &tm_h256 : &tm_h128, &a_full[as], kc * 64, (int)rb, pol_h);
+          const CUtensorMap* const tp =
+              NC > 1 ? (two ? mm_p<NC>(mm, c) : th) : (two ? &tm_h256 : &tm_h128);
+          tma_load_2d(dst, tp, &a_full[as], kc * 64, (int)rb, pol_h);
           if (++as == p.na) { as = 0; aph ^= 1; }
         };
         auto load_a = [&](int kc, int t) {
@@ -535,7 +557,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     while (next_group<NC>(it, c, g, r0, r1)) {
       const int T = (int)((r1 - r0 + 127) / 128);
       const float* const wup = NC > 1 ? p.wups[c] : sWup;
-      float* const scores_c = NC > 1 ? p.scores + (size_t)c * p.cap : p.scores;
+      float* const scores_c = (NC > 1 && p.scores) ? p.scores + (size_t)c * p.cap : p.scores;
       // sum of squares of this thread's row for each of its two tiles
       // (t = wset, wset + 2), four f32 chains each, from the swizzled A slots
       float ss[2][4];
@@ -681,7 +703,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const float score = score_from_logit(logit);
           const bool ex = valid && (score > p.theta);
           if (NC > 1) {
-            if (valid) scores_c[r] = score;
+            if (valid && scores_c) scores_c[r] = score;
+            if (ex && p.exit_layers) exit_min(p.exit_layers + (gathered ? p.row_idx[r] : r), p.layers[c]);
           } else if (valid) {
             if (p.scores) p.scores[r] = score;
             if (p.logits) p.logits[r] = logit;
@@ -1055,16 +1078,17 @@ int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   return tc_launch<1>(a, tm, mm, p, smem_bytes, grid, dev, stream, "route_tc_kernel");
 }
 
-// K1m: every row scored at C checkpoints in ONE persistent launch, scores to
-// a.scores[c * a.n + position]; dense (a.row_idx == NULL: rows 0..a.n-1 of
-// every capture) or gathered (the live rows a.row_idx[0 .. *a.n_dev), routed
-// only when a.n_min <= *a.n_dev <= n_limit).  The caller resolves the first
-// firing checkpoint per row (chain_resolve_launch).
+// K1m: every row scored at C checkpoints in ONE persistent launch; each row's
+// first firing checkpoint is combined in a.exit_layers by an atomic minimum
+// (rows that never fire keep NO_EXIT), scores optionally to a.scores[c *
+// a.n + position]; dense (a.row_idx == NULL: rows 0..a.n-1 of every capture)
+// or gathered (the live rows a.row_idx[0 .. *a.n_dev), routed only when
+// a.n_min <= *a.n_dev <= n_limit).
 int route_tc_multi_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
                           const void* const* w_ptrs, const float* const* wup_ptrs,
-                          int64_t n_limit, cudaStream_t stream) {
+                          const int64_t* layers, int64_t n_limit, cudaStream_t stream) {
   if (C < 2 || C > kMaxMC) return set_error(TIDE_ERR_UNSUPPORTED, "K1m: C must be in [2, %d]", kMaxMC);
-  if (!a.scores) return set_error(TIDE_ERR_ARG, "K1m: scores required");
+  if (!a.scores && !a.exit_layers) return set_error(TIDE_ERR_ARG, "K1m: scores or exit_layers required");
   if ((a.row_idx == nullptr) != (a.n_dev == nullptr))
     return set_error(TIDE_ERR_ARG, "K1m: row_idx and n_dev go together");
   int dev = 0;
@@ -1073,7 +1097,15 @@ int route_tc_multi_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
   TcParams p{};
   uint32_t smem_bytes = 0;
   int rc;
-  if ((rc = tc_params(a, false, p, smem_bytes))) return rc;
+  const bool gathered = a.row_idx != nullptr;
+  // dense: pair slots (two whole tiles of one checkpoint per 256-row box);
+  // TIDE_K1_PAIRSLOT=0 turns them off
+  bool pair = !gathered && std::min(4, 512 / (((a.b + 15) / 16 * 16 + 31) / 32 * 32)) == 4;
+  {
+    const char* env = getenv("TIDE_K1_PAIRSLOT");  // read per call
+    if (env) pair = pair && env[0] == '1';
+  }
+  if ((rc = tc_params(a, pair, p, smem_bytes))) return rc;
   p.gran = 128;
   p.nc = C;
   p.cap = a.n;
@@ -1082,9 +1114,8 @@ int route_tc_multi_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
   // scores only: no mask / logits / compaction / exit layers here
   p.logits = nullptr;
   p.mask = nullptr;
-  p.exit_idx = p.cont_idx = p.exit_layers = p.counts = nullptr;
+  p.exit_idx = p.cont_idx = p.counts = nullptr;  // exit_layers: first firing checkpoint (exit_min)
   p.inputs_ready = 0;
-  const bool gathered = a.row_idx != nullptr;
   const int64_t hrows = gathered ? a.rows_total : std::max<int64_t>(a.n, 1);
   static MultiMaps<kMaxMC> mm;  // host staging (copied into the launch parameters)
   static std::mutex mu;
@@ -1093,7 +1124,13 @@ int route_tc_multi_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
     if ((rc = make_map(&mm.h[c], h_ptrs[c], a.dtype, a.d, hrows, a.ld_h, 64, gathered ? 1 : 128)))
       return rc;
     if ((rc = make_map(&mm.w[c], w_ptrs[c], a.dtype, a.d, a.b, a.d, 64, p.npad))) return rc;
+    if (pair) {
+      if ((rc = make_map(&mm.p[c], h_ptrs[c], a.dtype, a.d, hrows, a.ld_h, 64, 256))) return rc;
+    } else {
+      mm.p[c] = mm.h[c];
+    }
     p.wups[c] = wup_ptrs[c];
+    p.layers[c] = layers[c];
   }
   CUtensorMap tm[7];
   for (int i = 0; i < 7; ++i) tm[i] = mm.h[0];

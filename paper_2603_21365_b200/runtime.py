@@ -501,12 +501,11 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
         # (K1m) + resolve: the first firing checkpoint is what peeling
         # computes (a row's score at checkpoint k depends only on that row)
         wts = [device_weights(bank.routers[k], code, dev) for k in ckpts]
-        scratch = torch.empty(len(ckpts) * n, dtype=torch.float32, device=dev)
         N.check(lib.tide_route_multi(
             N.ptr_array([staged[k + 1].data_ptr() for k in ckpts]), len(ckpts), d, n, None, n, d,
             code, None, N.ptr_array([w.data_ptr() for w, _ in wts]),
             N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(ckpts), eps, theta,
-            scratch.data_ptr(), exit_layers.data_ptr(), ws, s), "tide_route_multi")
+            None, exit_layers.data_ptr(), ws, s), "tide_route_multi")
         return exit_layers
     rem = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
     cnt = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(2)]

@@ -232,7 +232,7 @@ def run_configs(hbm_gbs: float, bf16_tflops: float):
     / peeled bytes), bf16 tensor peak for the LM head."""
     out = []
     for fn in (config1, lambda: config2(0.5), lambda: config2(1.0), config3, config4,
-               lambda: config5(0.7), lambda: config5(1.0), lm_head):
+               lambda: config5(0.5), lambda: config5(0.7), lambda: config5(1.0), lm_head):
         try:
             r = fn()
         except Exception as e:  # report, do not hide

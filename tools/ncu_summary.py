@@ -61,8 +61,10 @@ def short(name):
     base = m.group(1) if m else name.split("(")[0]
     if "<" in name.split("(")[0]:
         targ = name.split("<", 1)[1].split(">")[0]
-        if base == "route_tc_kernel":
-            return base + ("_bf16" if targ.strip() in ("1", "true") else "_f16")
+        if base == "route_tc_kernel":  # <kBF16, NC>: NC > 1 is K1m
+            a = [x.strip() for x in targ.split(",")]
+            return (base + ("_bf16" if a[0] in ("1", "true") else "_f16")
+                    + ("_k1m" if len(a) > 1 and a[1] != "1" else ""))
         if base == "route_tcs_kernel":  # <kBF16, NC>: NC > 1 is the chain tail
             return base + ("_tail" if targ.split(",")[-1].strip() not in ("1",) else "")
         if base == "lmhead_kernel":  # <kTerms>

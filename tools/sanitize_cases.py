@@ -99,7 +99,9 @@ def case_round2():
     os.environ["TIDE_F32_TC"] = "1"
     case_route("0", 600, 256, torch.float32)   # 3xTF32, segmented accumulators
     os.environ.pop("TIDE_F32_TC", None)
+    os.environ["TIDE_SPECULATIVE"] = "0"
     case_chain(700, 256, 24, 0.95)       # link 1 + the wide tail + resolve
+    os.environ.pop("TIDE_SPECULATIVE", None)
     from paper_2603_21365_b200 import _device as Dv
     from paper_2603_21365_b200 import _native as N
     lib = N.load()
@@ -117,15 +119,38 @@ def case_round2():
     assert np.array_equal(idx[: int(cnt[0])].cpu().numpy(), want)
 
 
-def main():
-    assert torch.cuda.is_available()
-    case_round2()
+def case_k1m():
+    """K1m (the whole per-token chain in one launch, exit map by atomic
+    minimum), dense with pair slots and gathered; K1 with several row groups
+    per CTA (the slot-release protocol), pair and single slots."""
+    os.environ["TIDE_SPECULATIVE"] = "1"
+    case_chain(1000, 512, 40, 0.6)      # dense K1m, ragged n, 10 checkpoints
+    os.environ.pop("TIDE_SPECULATIVE", None)
+    for pair in ("1", "0"):
+        os.environ["TIDE_K1_PAIRSLOT"] = pair
+        case_route("0", 148 * 640, 128)  # 5 tiles per CTA: two groups each
+    os.environ.pop("TIDE_K1_PAIRSLOT", None)
+
+
+def case_round1():
     case_route("0", 2000, 1024)          # persistent tcgen05 K1 (ragged tail)
     case_route("16", 1000, 2048)         # split-K cluster kernel
     case_route("0", 700, 768, torch.float32)  # CUDA-core f32 router
+    os.environ["TIDE_SPECULATIVE"] = "0"  # the peeling chain, not K1m
     st, bank, host = case_chain(1500, 512, 32, 0.55)  # peeling links + tail + resolve
+    os.environ.pop("TIDE_SPECULATIVE", None)
     case_project_label(st, bank, host)
-    print("sanitize cases ok")
+
+
+CASES = {"round1": case_round1, "round2": case_round2, "k1m": case_k1m}
+
+
+def main():
+    """python tools/sanitize_cases.py [round1|round2|k1m ...] (default: all)"""
+    assert torch.cuda.is_available()
+    for name in (sys.argv[1:] or list(CASES)):
+        CASES[name]()
+        print(f"sanitize cases ok: {name}")
 
 
 if __name__ == "__main__":

@@ -1020,16 +1020,24 @@ static int tc_launch(const RouteArgs& a, const CUtensorMap (&tm)[7], const Multi
   return check_launch(what);
 }
 
+// TIDE_K1_GRID (debug, read per call): run K1 / K1m as if the GPU had that
+// many SMs — several row groups per CTA at small sizes (compute-sanitizer).
+static int k1_sms(int dev) {
+  const char* env = getenv("TIDE_K1_GRID");
+  const int sms = sm_count(dev);
+  return env ? std::max(1, std::min(sms, atoi(env))) : sms;
+}
+
 int route_tc_launch(const RouteArgs& a, cudaStream_t stream) {
   int dev = 0;
   cudaGetDevice(&dev);
-  {
+  if (!getenv("TIDE_K1_GRID")) {
     // few rows: split d over a cluster instead (route_tcs.cu)
     int grid = 0;
     const int ks = route_tcs_plan(a, dev, &grid);
     if (ks) return route_tcs_launch(a, stream, ks, grid);
   }
-  const int sms = sm_count(dev);
+  const int sms = k1_sms(dev);
   // pair slots (two whole tiles per 32 KB slot: half the barrier round trips
   // per byte) for dense launches dealt in whole tiles; TIDE_K1_PAIRSLOT=0/1
   const int tpg0 = std::min(4, 512 / (((a.b + 15) / 16 * 16 + 31) / 32 * 32));
@@ -1093,7 +1101,7 @@ int route_tc_multi_launch(const RouteArgs& a, int C, const void* const* h_ptrs,
     return set_error(TIDE_ERR_ARG, "K1m: row_idx and n_dev go together");
   int dev = 0;
   cudaGetDevice(&dev);
-  const int sms = sm_count(dev);
+  const int sms = k1_sms(dev);
   TcParams p{};
   uint32_t smem_bytes = 0;
   int rc;

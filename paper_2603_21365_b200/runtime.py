@@ -318,7 +318,7 @@ class _ChainGraphs:
         import os
         e = os.environ
         return tuple(e.get(k) for k in ("TIDE_CHAIN_TAIL", "TIDE_TAIL_AFTER", "TIDE_TAIL_ROWS",
-                                        "TIDE_TAIL_WIDE", "TIDE_SPECULATIVE",
+                                        "TIDE_TAIL_WIDE", "TIDE_SPECULATIVE", "TIDE_WINDOW",
                                         "TIDE_TAIL_KS", "TIDE_SPLIT", "TIDE_PDL",
                                         "TIDE_F32_TAIL_ROWS"))
 
@@ -527,9 +527,32 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
     wide_at = 0 if (tails and len(ckpts) >= 3 and _tail_wide(theta)) else -1
     after = _tail_after()
     tail_at = after - 1 if (tails and len(ckpts) - after >= 2) else -1
+    start = _window(code, len(ckpts)) if wide_at < 0 else 0
+    if start:
+        # a speculative window: the first `start` checkpoints for every row
+        # in one K1m launch (no ordered look-back between them), then the
+        # survivors (exit code 0) compacted into the list the links peel
+        wts = [device_weights(bank.routers[k], code, dev) for k in ckpts[:start]]
+        N.check(lib.tide_route_multi(
+            N.ptr_array([staged[k + 1].data_ptr() for k in ckpts[:start]]), start, d, n, None, n,
+            d, code, None, N.ptr_array([w.data_ptr() for w, _ in wts]),
+            N.ptr_array([u.data_ptr() for _, u in wts]), b, N.i64_array(ckpts[:start]), eps,
+            theta, None, exit_layers.data_ptr(), ws, s), "tide_route_multi (window)")
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
+        N.check(lib.tide_exit_encode(exit_layers.data_ptr(), n, codes.data_ptr(), s),
+                "tide_exit_encode")
+        j = (start - 1) & 1  # the buffer link `start` reads (it writes the other)
+        N.check(lib.tide_compact(codes.data_ptr(), n, None, None, 0, None, 0, 0, 0, None,
+                                 rem[j].data_ptr(), None, None, cnt[j].data_ptr(), ws, s),
+                "tide_compact (window survivors)")
+        row_idx, n_dev = rem[j].data_ptr(), cnt[j].data_ptr() + 8
+        _chain_tail.keep = getattr(_chain_tail, "keep", ())[-4:] + (codes,)
+        tail_at = max(tail_at, start) if tail_at >= 0 else -1
     ls = s  # stream the links go to (a graph conditional's body after a tail)
     bodies = []
     for i, k in enumerate(ckpts):
+        if i < start:
+            continue
         wd, wu = device_weights(bank.routers[k], code, dev)
         h = staged[k + 1]
         N.check(lib.tide_route(h.data_ptr(), d, n, n_dev or None, n, d, code, row_idx or None,
@@ -575,6 +598,17 @@ def _speculative(n: int, d: int, final, theta: float) -> bool:
     if env is not None:
         return env == "1"
     return n * d * final.element_size() <= SPEC_BYTES or theta >= WIDE_THETA
+
+
+def _window(code, C: int) -> int:
+    """Checkpoints scored speculatively (one K1m launch) before the peeling
+    links start (TIDE_WINDOW; 0 = none)."""
+    import os
+    w = int(os.environ.get("TIDE_WINDOW", WINDOW))
+    return w if (code != N.F32 and 2 <= w < C and w <= MAX_MULTI_CKPTS) else 0
+
+
+WINDOW = 0
 
 
 def _tail_enabled() -> bool:

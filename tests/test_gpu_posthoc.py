@@ -260,6 +260,13 @@ def test_chain_tail_matches_oracle_and_links(d, n, L, scale, theta, monkeypatch)
         got = P.select_exits(states, bank, cfg).cpu().numpy()
         assert np.all((got == want) | exc), (wide, tail)
         out[wide + tail] = got
+    # a two-checkpoint speculative window, then the links (+ tail)
+    monkeypatch.setenv("TIDE_TAIL_WIDE", "0")
+    monkeypatch.setenv("TIDE_CHAIN_TAIL", "1")
+    monkeypatch.setenv("TIDE_WINDOW", "2")
+    out["win"] = P.select_exits(states, bank, cfg).cpu().numpy()
+    monkeypatch.delenv("TIDE_WINDOW")
+    assert np.all((out["win"] == want) | exc)
     monkeypatch.setenv("TIDE_SPECULATIVE", "1")
     out["spec"] = P.select_exits(states, bank, cfg).cpu().numpy()
     assert np.all((out["spec"] == want) | exc)

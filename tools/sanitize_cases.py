@@ -126,10 +126,12 @@ def case_k1m():
     os.environ["TIDE_SPECULATIVE"] = "1"
     case_chain(1000, 512, 40, 0.6)      # dense K1m, ragged n, 10 checkpoints
     os.environ.pop("TIDE_SPECULATIVE", None)
+    os.environ["TIDE_K1_GRID"] = "4"    # K1 as if on 4 SMs: several groups per CTA
     for pair in ("1", "0"):
         os.environ["TIDE_K1_PAIRSLOT"] = pair
-        case_route("0", 148 * 640, 128)  # 5 tiles per CTA: two groups each
+        case_route("0", 4 * 1152, 128)  # 9 tiles per CTA: three groups each
     os.environ.pop("TIDE_K1_PAIRSLOT", None)
+    os.environ.pop("TIDE_K1_GRID", None)
 
 
 def case_round1():

@@ -36,7 +36,7 @@ namespace tide {
 
 namespace {
 
-constexpr int kThreadsS = 192;  // producer, MMA issuer, 4 RMS / epilogue warps
+constexpr int kThreadsS = 320;  // producer, MMA issuer, 4 RMS / epilogue warps, 4 row gatherers
 constexpr int kMaxStages = 8;
 constexpr int kASlot = 128 * 128;  // 128 rows x 64 cols x 2 B
 
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     prefetch_tmap(&tm_w);
     if (p.row_idx == nullptr) prefetch_tmap(&tm_h);
     for (int i = 0; i < p.stages; ++i) {
-      // gathered: + one cp.async arrive per RMS thread (they copy the rows)
+      // gathered: + one cp.async arrive per gather thread (warps 6-9 copy the rows)
       mbar_init(&full[i], p.row_idx != nullptr ? 1 + 128 : 1);
       mbar_init(&empty[i], 1 + 4);  // MMA commit + the 4 RMS warps
     }
@@ -319,46 +319,12 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       __syncwarp();
       if (++s == p.stages) { s = 0; ph ^= 1u; }
     }
-  } else {
+  } else if (warp <= 5) {
     // ------------------------------------------------------------- RMS partials
     const int q = warp & 3;  // TMEM lane quadrant of this warp
     const int row = 32 * q + lane;
     const uint32_t swz = (uint32_t)(row & 7);
     float sq[4] = {0.f, 0.f, 0.f, 0.f};
-    const int nkr = k1 - k0;
-    // Gathered rows (TMA gather4 measured ~2.5x slower than this): cp.async,
-    // `stages` chunks ahead.  The warp copies its own 32 rows; one instruction moves 4
-    // rows x 128 B (8 lanes per row, 16 B each) so every L2 request is whole
-    // sectors.  Offsets of this lane's 8 rows (rows 32q + 4it + lane/8) are
-    // kept in registers (-1 = past the end: left unwritten, never used).
-    const int sub = lane & 7, rg = lane >> 3;
-    int64_t src_off[8];
-    if (gathered) {
-#pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int64_t r = r0 + 32 * q + 4 * it + rg;
-        src_off[it] = r < r1 ? p.row_idx[r] * p.ld_bytes : -1;
-      }
-    }
-    auto issue = [&](int i) {
-      const int si = i % p.stages;
-      mbar_wait(&empty[si], (((uint32_t)(i / p.stages)) & 1u) ^ 1u);
-      {
-        uint8_t* dst = smem + (size_t)si * p.stage_bytes;
-        const int64_t c = (int64_t)(k0 + i) * 64 + 8 * sub;  // this lane's 8 columns
-        const bool in = c < p.d;
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int rw = 32 * q + 4 * it + rg;
-          if (src_off[it] >= 0)
-            cp_async16(dst + rw * 128 + ((sub ^ (rw & 7)) << 4),
-                       h_base + src_off[it] + (in ? c * 2 : 0), in ? 16u : 0u);
-        }
-      }
-      cp_async_arrive_noinc(&full[si]);
-    };
-    if (gathered)
-      for (int i = 0; i < p.stages && i < nkr; ++i) issue(i);
     int s = 0;
     uint32_t ph = 0;
     for (int kc = k0; kc < k1; ++kc) {
@@ -378,9 +344,6 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       // LDS issue lets the refill race the reads, tools/stress_k1.py)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      // refill the previous chunk's slot (its MMA has had a whole chunk to retire)
-      const int i = kc - k0;
-      if (gathered && i >= 1 && i - 1 + p.stages < nkr) issue(i - 1 + p.stages);
       if (++s == p.stages) { s = 0; ph ^= 1u; }
     }
     const float ssp = (sq[0] + sq[1]) + (sq[2] + sq[3]);
@@ -428,14 +391,47 @@ __global__ void __launch_bounds__(kThreadsS, 1)
       }
       TL(5);
     }
+  } else if (gathered) {
+    // ------------------------------------------------------------- row gatherers
+    // Gathered rows by cp.async, warps 6-9 (one per SM sub-partition, 32
+    // rows each), issued as far ahead as the ring allows: they wait only for
+    // a stage's release (as the TMA producer does), not for the RMS reads of
+    // the chunk before.  One instruction moves 4 rows x 128 B (8 lanes per
+    // row, 16 B each) so every L2 request is whole sectors.  The byte
+    // offsets of a lane's 8 rows stay in registers (-1 = past the tile's
+    // live rows: left unwritten, never used).
+    const int gq = warp - 6;
+    const int sub = lane & 7, rg = lane >> 3;
+    int64_t src_off[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int64_t r = r0 + 32 * gq + 4 * it + rg;
+      src_off[it] = r < r1 ? p.row_idx[r] * p.ld_bytes : -1;
+    }
+    const int nkr = k1 - k0;
+    for (int j = 0; j < nkr; ++j) {
+      const int si = j % p.stages;
+      mbar_wait(&empty[si], (((uint32_t)(j / p.stages)) & 1u) ^ 1u);
+      uint8_t* dst = smem + (size_t)si * p.stage_bytes;
+      const int64_t c = (int64_t)(k0 + j) * 64 + 8 * sub;  // this lane's 8 columns
+      const bool in = c < p.d;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int rw = 32 * gq + 4 * it + rg;
+        if (src_off[it] >= 0)
+          cp_async16(dst + rw * 128 + ((sub ^ (rw & 7)) << 4), h_base + src_off[it] + (in ? c * 2 : 0),
+                     in ? 16u : 0u);
+      }
+      cp_async_arrive_noinc(&full[si]);
+    }
   }
-  if (warp < 2) {
+  if (warp < 2 || warp > 5) {
     cluster_arrive_relaxed();  // (the epilogue warps arrive once the ring is drained ...
     cluster_wait();
     cluster_arrive_relaxed();  // ... and once the partials of their rows landed)
   }
 
-  if (warp >= 2) {
+  if (warp >= 2 && warp <= 5) {
     if (live_rank) mbar_wait(recv_full, 0);
     // every copy INTO this CTA has landed; once all CTAs arrive, every copy
     // FROM this CTA's smem has been read, so it may exit

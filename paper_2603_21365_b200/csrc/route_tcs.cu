@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     unpack2(acc2, lo, hi);
     plog[sl * R + rr] = lo + hi;
     epi_bar();
+    if (threadIdx.x == 64) TL(10);
     // rows of this partition: threads t < R finish them (fixed slice order)
     const int64_t pr0 = r0 + (int64_t)rank * R;
     const int64_t pr1 = (pr0 + R < r1) ? pr0 + R : (pr0 < r1 ? r1 : pr0);
@@ -503,6 +504,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     const uint32_t bal = __ballot_sync(0xffffffffu, ex);
     if (lane == 0 && t < R) words[t >> 5] = bal;
     epi_bar();
+    if (threadIdx.x == 64) TL(11);
     if (warp == 2 && (p.exit_idx || p.cont_idx || p.counts)) {
       const int nw = (R + 31) / 32;
       const uint32_t word = lane < nw ? words[lane] : 0u;

@@ -51,7 +51,8 @@ live = t[:, 0] > 0
 t = t[live]
 t0 = t[:, 0].min()
 names = {0: "entry", 1: "setup_done", 2: "producer_issued", 3: "rms_done", 4: "acc_full",
-         5: "pushed", 6: "cluster_sync1", 7: "cluster_sync2", 8: "lookback_done", 9: "end"}
+         5: "pushed", 6: "cluster_sync1", 10: "logit_partials", 11: "finished_rows",
+         8: "lookback_done", 7: "cluster_sync2", 9: "end"}
 print(f"{t.shape[0]} CTAs; us relative to first CTA entry: min / median / max")
 for k, nm in names.items():
     v = t[:, k]

@@ -31,6 +31,11 @@ namespace tide {
 
 namespace {
 
+#ifndef TIDE_DEC_EXP
+#define TIDE_DEC_EXP 0  // timing experiments only (wrong results, tools/decode_exp.py): 1 one
+                        // W chunk per slice, 2 no resolution atomic, 3 no row loads, 4 no
+                        // DSMEM exchange
+#endif
 constexpr int kDThreads = 256;
 constexpr int kDWarps = kDThreads / 32;
 constexpr int kDMaxRows = TIDE_MAX_DECODE_ROWS;
@@ -296,6 +301,10 @@ __device__ __forceinline__ void decode_resolve_row(const DecParams& p, int c, in
   }
   constexpr unsigned long long kOne = 1ull << 56, kBits = kOne - 1ull;
   const unsigned long long add = kOne | (fired ? (1ull << c) : 0ull);
+  if (TIDE_DEC_EXP == 2) {
+    if (p.exit_layers && c == 0) p.exit_layers[r] = fired;
+    return;
+  }
   const unsigned long long old = atom_add_relaxed_u64(&p.ws->dec_rows[r], add);
   if (p.scores) p.scores[(int64_t)c * n + r] = score_from_logit(t);
   if (p.logits) p.logits[(int64_t)c * n + r] = t;
@@ -471,7 +480,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   // the previous kernel runs, so by the time the rows land W is resident and
   // a single wait precedes the whole MMA stream (a wait per k-chunk cost
   // ~500 cycles each, measured).
-  const int nkc_mma = p.w_packed ? min(nkc, p.nk - c0 / 64) : nkc;  // packed: chunks past d skipped
+  const int nkc_mma = TIDE_DEC_EXP == 1 ? 1 : p.w_packed ? min(nkc, p.nk - c0 / 64) : nkc;  // packed: chunks past d skipped
   if (p.w_packed) {
     // the pre-swizzled image: one 1-D bulk copy (MT x 16 KB) per k-chunk
     if (threadIdx.x == 0) {
@@ -520,7 +529,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
   // are touched only after it completed.
   griddep_wait();
   DTL(12);
-  for (int i = threadIdx.x; i < 16 * per_row; i += kDThreads) {
+  for (int i = threadIdx.x; TIDE_DEC_EXP != 3 && i < 16 * per_row; i += kDThreads) {
     const int r = i / per_row, rem = i - r * per_row, kc = rem >> 3, q = rem & 7;
     const int col = c0 + kc * 64 + q * 8;
     const bool in = col < p.d && r < n;
@@ -624,7 +633,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
     // completed here, measured), then each sending lane issues its copy
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // sRows -> bulk copy reads
     cluster_wait();
-    if (lane < n && (lane % S) != (int)rank) {
+    if (TIDE_DEC_EXP != 4 && lane < n && (lane % S) != (int)rank) {
       const int r = lane, q = r % S, k = r / S;
       const uint32_t dst = dsmem_addr(smem_u32(recv + ((size_t)k * S + rank) * RB), (uint32_t)q);
       const uint32_t bar = dsmem_addr(smem_u32(recv_bar), (uint32_t)q);
@@ -654,7 +663,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_tc_kernel(const __grid_co
     }
   }
 #endif
-  mbar_wait_spin(recv_bar, 0);
+  if (TIDE_DEC_EXP != 4) mbar_wait_spin(recv_bar, 0);
   DTL(3);
   // 4. rows owned here (k = 0 .. own_rows - 1, row r = rank + k S), 128
   //    threads per row, unit j per thread: totals over the S slices in fixed
@@ -1061,8 +1070,11 @@ extern "C" int tide_route_decode_ex(const void* const* h_ptrs, int32_t C, int64_
   // reduction) when S <= 16 and all C clusters fit; TIDE_DECODE_CLUSTER=0 disables
   const char* cenv = getenv("TIDE_DECODE_CLUSTER");  // read per call (tests switch it)
   if (tc && C <= kAtomicMaxC && !(cenv && cenv[0] == '0')) {
-    // widest slice first (S = 16, then 8): fewer bytes per CTA, if co-resident
-    for (int cw = cs; cw <= 4 * cs; cw *= 2) {
+    // widest slice first (S = 16, then 8): fewer bytes per CTA, if co-resident;
+    // TIDE_DECODE_COLS (a multiple of 64, read per call) tries that width only
+    const char* wenv = getenv("TIDE_DECODE_COLS");
+    const int cw0 = wenv ? std::max(64, atoi(wenv) / 64 * 64) : cs;
+    for (int cw = cw0; cw <= (wenv ? cw0 : 4 * cs); cw *= 2) {
       DecParams q = p;
       q.cs = cw;
       q.S = (d + cw - 1) / cw;

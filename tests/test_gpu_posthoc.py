@@ -524,3 +524,23 @@ def test_route_multi_dense_and_gathered(d, n, L, dtype):
     assert np.all((gl[sel] == want[sel]) | exc[sel])
     others = np.setdiff1d(np.arange(n), sel)
     assert np.all(gl[others] == P.NO_EXIT)
+
+
+def test_speculative_chain_repeats_bitwise():
+    """K1m (exit map by atomic minimum across CTAs): repeated select_exits
+    calls on the same captures give the same exit map, with L2-thrashing
+    writes in between (the minimum does not depend on arrival order)."""
+    need_gpu()
+    import os
+    ckpts, routers, states, bank, head = _big_case(32, 4096, 4096, "bf16", 77, scale=0.1)
+    cfg = P.RuntimeConfig(exit_threshold=0.6)
+    os.environ["TIDE_SPECULATIVE"] = "1"
+    try:
+        want = P.select_exits(states, bank, cfg).clone()
+        junk = torch.empty(1 << 26, device="cuda")
+        for i in range(20):
+            junk.fill_(float(i))
+            assert torch.equal(P.select_exits(states, bank, cfg), want), i
+    finally:
+        os.environ.pop("TIDE_SPECULATIVE", None)
+    assert (want >= 0).any() and len(torch.unique(want)) > 2

@@ -62,10 +62,13 @@ def case_chain(n, d, L, theta):
         exc |= np.abs(t - O.logit_of(theta)) <= 2e-2 * np.maximum(np.abs(t), m)
     want = O.first_exit_from_scores(scores, theta)
     assert np.all((got == want) | exc)
-    # decode step (every checkpoint in one launch) on the first rows
-    dec = [s[:8].contiguous() for s in states]
-    got8 = P.select_exits(dec, bank, P.RuntimeConfig(exit_threshold=theta)).cpu().numpy()
-    assert np.all((got8 == want[:8]) | exc[:8])
+    # decode step (every checkpoint in one launch) on the first rows; skipped
+    # by SANITIZE_NO_DECODE=1 (under racecheck its cluster peers run so slowly
+    # that the spin-limit trap fires; the decode has its own racecheck run)
+    if os.environ.get("SANITIZE_NO_DECODE") != "1":
+        dec = [s[:8].contiguous() for s in states]
+        got8 = P.select_exits(dec, bank, P.RuntimeConfig(exit_threshold=theta)).cpu().numpy()
+        assert np.all((got8 == want[:8]) | exc[:8])
     os.environ.pop("TIDE_CHAIN_GRAPHS", None)
     return states, bank, host
 

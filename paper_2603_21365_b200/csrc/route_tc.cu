@@ -756,8 +756,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const int par = gi & 1;
       mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&m_empty[par]);
       const uint32_t cnt = __popc(word);
       uint32_t incl = cnt;
 #pragma unroll
@@ -767,6 +765,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       const uint32_t excl_w = incl - cnt;
       const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+      // the words buffer is released only once the scan consumed the loaded
+      // words (an arrive right after the load issue let the epilogue of the
+      // group two ahead overwrite it first: compute-sanitizer racecheck)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m_empty[par]);
       if (dbg && lane == 0) dbg[4] = gtimer();
       if (need_scan) {
         const uint32_t E = lookback_exclusive(p.ws->status, tag, g, agg);

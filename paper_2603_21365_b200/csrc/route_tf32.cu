@@ -456,8 +456,6 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
       const int par = gi & 1;
       mbar_wait(&m_full[par], ((uint32_t)gi >> 1) & 1u);
       const uint32_t word = lane < 16 ? words[par * 16 + lane] : 0u;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&m_empty[par]);
       const uint32_t c = __popc(word);
       uint32_t incl = c;
 #pragma unroll
@@ -467,6 +465,11 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
       }
       const uint32_t excl_w = incl - c;
       const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+      // the words buffer is released only once the scan consumed the loaded
+      // words (an arrive right after the load issue let the epilogue of the
+      // group two ahead overwrite it first: compute-sanitizer racecheck)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m_empty[par]);
       if (need_scan) {
         const uint32_t E = lookback_exclusive(p.ws->status, tag, g, agg);
         if (p.exit_idx || p.cont_idx) {

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -180,6 +181,216 @@ __global__ void __launch_bounds__(kLThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair form (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256-row x 256-vocab tile with M = 256 MMAs issued by the leader.  CTA r
+// stages its own 128 rows of A and HALF of the vocab tile's B rows (v0 + 128 r
+// ..), so each SM streams 64 KB per 64-column chunk (3-term) instead of 96 KB:
+// the one-CTA kernel is fed from L2 (A re-read by every vocab tile, B by
+// every row tile) and the halved B share is what the pair buys.  The peer
+// forwards "my stage landed" to the leader (remote mbarrier arrive); the
+// leader's commits arrive on both CTAs' barriers (multicast).  Each CTA's
+// TMEM holds its own 128 rows x 256 columns (big, + small at column 256):
+// the epilogue is the one-CTA kernel's.
+__device__ __forceinline__ uint32_t lm_cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t lm_mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void lm_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+__device__ __forceinline__ void lm_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void lm_tmem_alloc2(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void lm_tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void lm_mma2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit -> one arrive on the barrier at this smem offset in BOTH CTAs of the pair
+__device__ __forceinline__ void lm_commit2_both(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], m;\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int kTerms>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLThreads, 1)
+    lmhead2_kernel(const __grid_constant__ CUtensorMap tm_ah, const __grid_constant__ CUtensorMap tm_al,
+                   const __grid_constant__ CUtensorMap tm_bh, const __grid_constant__ CUtensorMap tm_bl,
+                   const __grid_constant__ LmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes);
+  uint64_t* full = bars;             // this CTA's stage landed (TMA bytes)
+  uint64_t* peer_full = bars + 8;    // leader: the peer's stage landed (forwarded)
+  uint64_t* empty = bars + 16;       // both: stage consumed (leader's commit, multicast)
+  uint64_t* acc_full = bars + 24;    // both: accumulator complete (multicast)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = lm_cta_rank();
+  const bool leader = rank == 0;
+  const int64_t m0 = (int64_t)blockIdx.x * kLBM;                     // this CTA's 128 rows
+  const int64_t v0 = (int64_t)blockIdx.y * kLBN;                     // the pair's 256 vocab columns
+  const int64_t vb = v0 + (int64_t)rank * (kLBN / 2);               // this CTA's B half
+  constexpr uint32_t kHalfB = (kLBN / 2) * 128;                     // 16 KB
+  const uint32_t cols = kTerms == 3 ? 512u : 256u;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_ah);
+    prefetch_tmap(&tm_bh);
+    if (kTerms == 3) {
+      prefetch_tmap(&tm_al);
+      prefetch_tmap(&tm_bl);
+    }
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&peer_full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) lm_tmem_alloc2(tmem_slot, cols);
+  tc_fence_before();
+  __syncthreads();
+  lm_cluster_sync();  // the peer's barriers exist before any remote arrive / multicast
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // the staged rows may come from the kernel just before on the stream
+
+  if (warp == 0) {
+    // ----------------------------------------------------------- producer (both CTAs)
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();
+      uint64_t pol_b;
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_b));
+      const uint32_t bytes = kTerms == 3 ? 2u * (kLASlot + kHalfB) : kLASlot + kHalfB;
+      for (int kc = 0; kc < p.nk; ++kc) {
+        const int s = kc % p.stages;
+        mbar_wait(&empty[s], ((kc / p.stages) & 1) ^ 1);
+        uint8_t* st = smem + (size_t)s * p.stage_bytes;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_load_2d(st, &tm_ah, &full[s], kc * kLBK, (int)m0, pol_a);
+        tma_load_2d(st + kLASlot, &tm_bh, &full[s], kc * kLBK, (int)vb, pol_b);
+        if (kTerms == 3) {
+          tma_load_2d(st + kLASlot + kHalfB, &tm_al, &full[s], kc * kLBK, (int)m0, pol_a);
+          tma_load_2d(st + 2 * kLASlot + kHalfB, &tm_bl, &full[s], kc * kLBK, (int)vb, pol_b);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader) {
+      // ----------------------------------------------------------- MMA issuer (leader)
+      const uint64_t dh = sw128_kmajor_desc(0);
+      for (int kc = 0; kc < p.nk; ++kc) {
+        const int s = kc % p.stages;
+        const uint32_t ph = (kc / p.stages) & 1;
+        mbar_wait(&full[s], ph);
+        mbar_wait(&peer_full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint8_t* st = smem + (size_t)s * p.stage_bytes;
+          const uint64_t ah = dh | (uint64_t)((smem_u32(st) & 0x3FFFFu) >> 4);
+          const uint64_t bh = dh | (uint64_t)((smem_u32(st + kLASlot) & 0x3FFFFu) >> 4);
+          const uint64_t al = dh | (uint64_t)((smem_u32(st + kLASlot + kHalfB) & 0x3FFFFu) >> 4);
+          const uint64_t bl = dh | (uint64_t)((smem_u32(st + 2 * kLASlot + kHalfB) & 0x3FFFFu) >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acc = (kc != 0 || k != 0) ? 1u : 0u;
+            lm_mma2(tmem_base, ah + 2 * k, bh + 2 * k, p.idesc, acc);
+            if (kTerms == 3) {
+              lm_mma2(tmem_base + 256u, ah + 2 * k, bl + 2 * k, p.idesc, acc);
+              lm_mma2(tmem_base + 256u, al + 2 * k, bh + 2 * k, p.idesc, 1u);
+            }
+          }
+          lm_commit2_both(&empty[s]);
+          if (kc == p.nk - 1) lm_commit2_both(acc_full);
+        }
+        __syncwarp();
+      }
+    } else if (lane == 0) {
+      // ----------------------------------------------------------- peer: forward "landed"
+      const uint32_t remote = lm_mapa(smem_u32(peer_full), 0);
+      for (int kc = 0; kc < p.nk; ++kc) {
+        const int s = kc % p.stages;
+        mbar_wait(&full[s], (kc / p.stages) & 1);
+        lm_arrive_remote(remote + (uint32_t)s * 8u);
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;  // TMEM lane quadrant
+    const int64_t row = m0 + 32 * q + lane;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16);
+    float* orow = p.out + row * p.ld_out;
+    for (int c0 = 0; c0 < kLBN; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(taddr + (uint32_t)c0, v);
+      tmem_ld_wait_regs(v);
+      if (kTerms == 3) {
+        uint32_t w[32];
+        tmem_ld32(taddr + 256u + (uint32_t)c0, w);
+        tmem_ld_wait_regs(w);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+      }
+      if (row < p.n) {
+        const int64_t col = v0 + c0;
+        if (col + 32 <= p.V) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(orow + col + j) =
+                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                            __uint_as_float(v[j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col + j < p.V) orow[col + j] = __uint_as_float(v[j]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  lm_cluster_sync();  // neither CTA leaves (or frees TMEM) while the pair's MMAs / copies may touch it
+  if (warp == 1) {
+    tc_fence_after();
+    lm_tmem_dealloc2(tmem_base, cols);
+  }
+}
+
+bool lm_pair(int terms) {
+  const char* env = getenv("TIDE_LM_PAIR");  // read per call
+  if (env) return env[0] == '1';
+  return terms == 3;
+}
+
 }  // namespace
 
 int lmhead_launch(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, int32_t d,
@@ -189,36 +400,45 @@ int lmhead_launch(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, i
   CUtensorMap ah, al, bh, bl;
   int rc;
   if ((rc = make_map(&ah, a_hi, TIDE_BF16, d, n, ld_a, kLBK, kLBM))) return rc;
-  if ((rc = make_map(&bh, b_hi, TIDE_BF16, d, V, ld_b, kLBK, kLBN))) return rc;
+  const int bbox = lm_pair(terms) ? kLBN / 2 : kLBN;  // pair: each CTA loads half of B
+  if ((rc = make_map(&bh, b_hi, TIDE_BF16, d, V, ld_b, kLBK, bbox))) return rc;
   if (terms == 3) {
     if ((rc = make_map(&al, a_lo, TIDE_BF16, d, n, ld_a, kLBK, kLBM))) return rc;
-    if ((rc = make_map(&bl, b_lo, TIDE_BF16, d, V, ld_b, kLBK, kLBN))) return rc;
+    if ((rc = make_map(&bl, b_lo, TIDE_BF16, d, V, ld_b, kLBK, bbox))) return rc;
   } else {
     al = ah;
     bl = bh;
   }
+  // CTA pairs for the 3-term (f32-grade) form: 3.87 -> 3.41 ms at 4,096 x
+  // 50,257 x 4096; the hi-only form stays on one CTA (1.59 vs 1.74 ms).
+  // TIDE_LM_PAIR=0 / 1 forces either.
+  const bool pair = lm_pair(terms);
   LmParams p{};
   p.n = n;
   p.V = V;
   p.ld_out = ld_out;
   p.nk = (d + kLBK - 1) / kLBK;
   p.terms = terms;
-  p.stage_bytes = terms == 3 ? 2u * (kLASlot + kLBSlot) : kLASlot + kLBSlot;
+  p.stage_bytes = pair ? (terms == 3 ? 2u * (kLASlot + kLBSlot / 2) : kLASlot + kLBSlot / 2)
+                       : (terms == 3 ? 2u * (kLASlot + kLBSlot) : kLASlot + kLBSlot);
   const uint32_t cap = 227u * 1024u - 1024u - 256u;
   p.stages = (int)std::min<uint32_t>(8u, cap / p.stage_bytes);
-  p.idesc = f16_idesc(1, kLBM, kLBN);
+  p.idesc = f16_idesc(1, pair ? 2 * kLBM : kLBM, kLBN);
   p.out = out;
   const uint32_t smem = (uint32_t)p.stages * p.stage_bytes + 256u + 1024u;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(lmhead_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(lmhead_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(lmhead2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(lmhead2_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int64_t gy = (V + kLBN - 1) / kLBN;
   if (gy > 65535) return set_error(TIDE_ERR_UNSUPPORTED, "tide_lm_head: vocab too large (%lld)", (long long)V);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((n + kLBM - 1) / kLBM), (unsigned)gy, 1);
+  const int64_t gx = pair ? 2 * ((n + 2 * kLBM - 1) / (2 * kLBM)) : (n + kLBM - 1) / kLBM;
+  cfg.gridDim = dim3((unsigned)gx, (unsigned)gy, 1);
   cfg.blockDim = dim3(kLThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -227,8 +447,11 @@ int lmhead_launch(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, i
   attr1[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr1;
   cfg.numAttrs = 1;
-  const cudaError_t e = terms == 3 ? cudaLaunchKernelEx(&cfg, lmhead_kernel<3>, ah, al, bh, bl, p)
-                                   : cudaLaunchKernelEx(&cfg, lmhead_kernel<1>, ah, al, bh, bl, p);
+  const cudaError_t e =
+      pair ? (terms == 3 ? cudaLaunchKernelEx(&cfg, lmhead2_kernel<3>, ah, al, bh, bl, p)
+                         : cudaLaunchKernelEx(&cfg, lmhead2_kernel<1>, ah, al, bh, bl, p))
+           : (terms == 3 ? cudaLaunchKernelEx(&cfg, lmhead_kernel<3>, ah, al, bh, bl, p)
+                         : cudaLaunchKernelEx(&cfg, lmhead_kernel<1>, ah, al, bh, bl, p));
   if (e != cudaSuccess) return set_error(TIDE_ERR_CUDA, "lmhead_kernel: %s", cudaGetErrorString(e));
   return check_launch("lmhead_kernel");
 }

@@ -41,10 +41,15 @@ def _lm(a32, b32, terms):
     return out[:, :V].cpu().numpy()
 
 
+@pytest.mark.parametrize("pair", ["1", "0"])
 @pytest.mark.parametrize("n,d,V", [(1, 64, 64), (8, 4096, 1000), (130, 772, 300),
-                                   (1000, 1024, 2500), (300, 4096, 50257)])
-def test_lm_head_three_terms_f32_grade(n, d, V):
+                                   (1000, 1024, 2500), (300, 4096, 50257), (129, 256, 129)])
+def test_lm_head_three_terms_f32_grade(n, d, V, pair, monkeypatch):
+    """Both forms: CTA pairs (cta_group::2, the default for 3 terms; ragged
+    row counts leave the pair's second CTA partly or wholly past the rows)
+    and the one-CTA kernel."""
     need_gpu()
+    monkeypatch.setenv("TIDE_LM_PAIR", pair)
     g = np.random.Generator(np.random.PCG64(n + d + V))
     a = g.standard_normal((n, d), dtype=np.float32)
     b = (g.standard_normal((V, d)) * 0.02).astype(np.float32)
@@ -59,8 +64,10 @@ def test_lm_head_three_terms_f32_grade(n, d, V):
     assert np.abs(got - f32).max() <= 4 * np.abs(f32 - exact).max() + 1e-5 * M.max()
 
 
-def test_lm_head_hi_only_bf16_products():
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_lm_head_hi_only_bf16_products(pair, monkeypatch):
     need_gpu()
+    monkeypatch.setenv("TIDE_LM_PAIR", pair)
     g = np.random.Generator(np.random.PCG64(5))
     a = g.standard_normal((257, 512), dtype=np.float32)
     b = (g.standard_normal((600, 512)) * 0.02).astype(np.float32)

@@ -110,11 +110,11 @@ def test_reference_bank_object_is_accepted(golden_posthoc):
     np.testing.assert_array_equal(e1, e2)
 
 
-def _big_case(L, d, n, dtype, seed, scale=0.1):
+def _big_case(L, d, n, dtype, seed, scale=0.1, b=128):
     """Synthetic capture + bank at a BASELINE config shape (device tensors)."""
     g = np.random.Generator(np.random.PCG64(seed))
     ckpts = O.checkpoint_layers(L, 4)
-    routers = {k: O.make_router(d, 128, k, g, scale=scale) for k in ckpts}
+    routers = {k: O.make_router(d, b, k, g, scale=scale) for k in ckpts}
     tdt = {"bf16": torch.bfloat16, "f16": torch.float16}[dtype]
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
@@ -544,3 +544,25 @@ def test_speculative_chain_repeats_bitwise():
     finally:
         os.environ.pop("TIDE_SPECULATIVE", None)
     assert (want >= 0).any() and len(torch.unique(want)) > 2
+
+
+@pytest.mark.parametrize("d,n,L,b", [(776, 1000, 24, 128), (1024, 3000, 20, 256), (512, 700, 16, 64)])
+def test_speculative_chain_odd_shapes(d, n, L, b, monkeypatch):
+    """K1m through select_exits at shapes off the main configs: d not a
+    multiple of 64 (partial last chunk), bottleneck 256 (two tiles per
+    group) and 64 (narrow N) -- the oracle's per-token map (band rule)."""
+    need_gpu()
+    monkeypatch.setenv("TIDE_SPECULATIVE", "1")
+    ckpts, routers, states, bank, head = _big_case(L, d, n, "bf16", 5 + d + b, scale=0.15, b=b)
+    cfg = P.RuntimeConfig(exit_threshold=0.6)
+    got = P.select_exits(states, bank, cfg).cpu().numpy()
+    scores, exc = {}, np.zeros(n, bool)
+    for k in ckpts:
+        s_, t, m = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
+        scores[k] = s_
+        exc |= np.abs(t - O.logit_of(0.6)) <= RTOL["bf16"] * np.maximum(np.abs(t), m)
+    want = O.first_exit_from_scores(scores, 0.6)
+    assert np.all((got == want) | exc)
+    monkeypatch.setenv("TIDE_SPECULATIVE", "0")
+    peel = P.select_exits(states, bank, cfg).cpu().numpy()
+    assert np.all((peel == want) | exc)

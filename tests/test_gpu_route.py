@@ -55,6 +55,26 @@ def test_route_case_matches_oracle_and_golden(golden_route, name):
             assert scores[i] == want, (i, scores[i], want)
 
 
+@pytest.mark.parametrize("name", sorted(ROUTE_CASES))
+def test_route_scores_matches_reference_composed(golden_route, name):
+    """route_scores (the composed equivalence partner, ee/router_ops.py:60-65)
+    on the device against the REFERENCE's own composed scores recorded in
+    the golden fixture (not against the fused kernel): within 1e-5 (f32
+    products) for f32 inputs, the bf16 band for bf16 / f16 captures."""
+    need_gpu()
+    key = f"{name}__composed"
+    if key not in golden_route.files:
+        pytest.skip("no composed vector recorded for this case")
+    spec = ROUTE_CASES[name]
+    h, wd, wu = make_route_inputs(spec)
+    want = golden_route[key]
+    got = P.route_scores(to_dev(h, spec["dtype"]), _router(wd, wu))
+    got = got.cpu().numpy() if hasattr(got, "cpu") else np.asarray(got)
+    tol = 1e-5 if spec["dtype"] == "f32" else 2e-2
+    assert got.shape == want.shape
+    assert np.max(np.abs(got.astype(np.float64) - want)) <= tol
+
+
 @pytest.mark.parametrize("theta", [1.0, 0.85, 0.5, 0.1])
 def test_threshold_rule_and_off_switch(theta):
     need_gpu()

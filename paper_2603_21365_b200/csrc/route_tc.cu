@@ -145,13 +145,6 @@ struct GroupIter {
 #ifndef TIDE_K1_PROFILE
 #define TIDE_K1_PROFILE 0
 #endif
-#ifndef TIDE_K1_GROUPBAR
-#define TIDE_K1_GROUPBAR 0  // debug: all roles meet at the end of every group
-#endif
-#define K1_GROUP_END()                                                     \
-  do {                                                                     \
-    if (TIDE_K1_GROUPBAR) asm volatile("barrier.sync 1, %0;" ::"r"(kThreadsTC)); \
-  } while (0)
 __device__ __forceinline__ long long pclk() {
 #if TIDE_K1_PROFILE
   return clock64();
@@ -426,7 +419,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
         }
       }
-      K1_GROUP_END();
     }
     if (dbg && lane == 0) { dbg[1] = gtimer(); dbg[18] = pw_cyc; dbg[19] = pclk() - p_begin; }
   } else if (warp == 1) {
@@ -535,7 +527,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int j = 0; j < p.nx; ++j)
         if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
       accph ^= (1u << T) - 1u;
-      K1_GROUP_END();
     }
     if (dbg && lane == 0) { dbg[16] = wait_cyc; dbg[17] = pclk() - t_begin; }
   } else if (warp <= 9) {
@@ -742,7 +733,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (dbg && warp == 2 && lane == 0) dbg[3] = gtimer();
       if (lane == 0) mbar_arrive(&m_full[par]);
       ++gi;
-      K1_GROUP_END();
     }
   } else {
     // ----------------------------------------------------------- compaction
@@ -798,7 +788,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
       }
       ++gi;
-      K1_GROUP_END();
     }
     if (NC == 1 && NG == 0 && blockIdx.x == 0 && lane == 0 && p.counts) {
       p.counts[0] = 0;

@@ -69,7 +69,7 @@ def _strategy(ckpts, n, d, states, theta, gms):
     speculative (K1m: every row at every checkpoint, 2 launches) or peeling
     (one link per checkpoint, live rows only)."""
     from paper_2603_21365_b200 import runtime as R
-    spec = len(ckpts) <= R.MAX_MULTI_CKPTS and R._speculative(n, d, states[-1], theta)
+    spec = len(ckpts) <= R.MAX_MULTI_CKPTS and R._speculative(n, d, states[-1], theta, len(ckpts))
     if not spec:
         return {"strategy": "peeling", "launches": len(ckpts)}
     read = len(ckpts) * (n * (d * 2 + 4) + 128 * d * 2 + 512)

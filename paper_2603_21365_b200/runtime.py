@@ -496,7 +496,8 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
         if rc == 0:
             return exit_layers
         # a shape the one-launch tail does not take: the per-checkpoint links below
-    if code != N.F32 and 2 <= len(ckpts) <= MAX_MULTI_CKPTS and _speculative(n, d, final, theta):
+    if (code != N.F32 and 2 <= len(ckpts) <= MAX_MULTI_CKPTS
+            and _speculative(n, d, final, theta, len(ckpts))):
         # every row at every checkpoint in ONE persistent tensor-core launch
         # (K1m) + resolve: the first firing checkpoint is what peeling
         # computes (a row's score at checkpoint k depends only on that row)
@@ -581,23 +582,25 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
 
 TAIL_AFTER = 3  # links of the peeling chain before the tail attempt
 MAX_MULTI_CKPTS = 24  # route_tc.cu kMaxMC
-SPEC_BYTES = 64 << 20  # per-checkpoint capture bytes up to which scoring is speculative
+SPEC_BYTES = 320 << 20  # all captures' bytes up to which scoring is speculative
 
 
-def _speculative(n: int, d: int, final, theta: float) -> bool:
+def _speculative(n: int, d: int, final, theta: float, C: int) -> bool:
     """Score every checkpoint for every row in one launch (tide_route_multi)
     instead of peeling?  Peeling reads only the live rows but pays one
     latency-bound link per checkpoint (~15-20 us at 4,096 x 4096, mostly
-    fixed cost); speculation reads every capture once at the streaming rate.
-    Taken when a checkpoint's capture is small enough that its bytes cost less
-    than a link's fixed cost (n d e <= SPEC_BYTES: configs 1-2-sized
-    prefills), or when few rows exit anyway (theta >= WIDE_THETA).
+    fixed cost, and a few us even when nearly empty); speculation reads every
+    capture once at the streaming rate (~5-6 TB/s).  Taken when all C
+    captures together are small (C n d e <= SPEC_BYTES, ~60 us of streaming:
+    config-2-sized prefills, where even a chain whose rows all leave at the
+    first checkpoint costs about as much), or when few rows exit anyway
+    (theta >= WIDE_THETA: peeling would read nearly everything too).
     TIDE_SPECULATIVE=1 / 0 forces it on / off."""
     import os
     env = os.environ.get("TIDE_SPECULATIVE")
     if env is not None:
         return env == "1"
-    return n * d * final.element_size() <= SPEC_BYTES or theta >= WIDE_THETA
+    return C * n * d * final.element_size() <= SPEC_BYTES or theta >= WIDE_THETA
 
 
 def _window(code, C: int) -> int:

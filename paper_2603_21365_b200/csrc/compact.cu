@@ -142,6 +142,45 @@ __global__ void __launch_bounds__(kCThreads) compact_kernel(const CompactParams 
   if (tid == 0) launch_done(p.ws);
 }
 
+// Row gather from the index lists the scan wrote (dense rows): output row j
+// is rows[exit_idx[j]] for j < counts[0], else rows[cont_idx[j - counts[0]]]
+// into the continuing block.  A warp per output row with 8 16-byte loads in
+// flight per lane, every SM busy (the scan's own warp-per-row gather runs on
+// one CTA per 2,048-row partition: 32 CTAs at 65,536 rows, 0.5 TB/s).
+__global__ void __launch_bounds__(256) gather_rows_kernel(
+    const int64_t* __restrict__ exit_idx, const int64_t* __restrict__ cont_idx,
+    const int64_t* __restrict__ counts, const uint8_t* __restrict__ rows, int64_t pitch,
+    int64_t row_bytes, uint8_t* __restrict__ exit_rows, uint8_t* __restrict__ cont_rows) {
+  griddep_wait();  // the scan kernel just before wrote the indices and counts
+  const int64_t ne = counts[0], nt = counts[0] + counts[1];
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (row_bytes % 16 == 0) && (pitch % 16 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(exit_rows) |
+                     reinterpret_cast<uintptr_t>(cont_rows)) & 15) == 0;
+  for (int64_t j = wid; j < nt; j += nw) {
+    const bool ex = j < ne;
+    if (ex ? exit_rows == nullptr : cont_rows == nullptr) continue;
+    const int64_t src_row = ex ? exit_idx[j] : cont_idx[j - ne];
+    const uint8_t* src = rows + src_row * pitch;
+    uint8_t* dst = ex ? exit_rows + j * row_bytes : cont_rows + (j - ne) * row_bytes;
+    if (vec) {
+      for (int64_t o0 = (int64_t)lane * 16; o0 < row_bytes; o0 += 32 * 16 * 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (o0 + u * 512 < row_bytes) v[u] = ld_nc_v4(src + o0 + u * 512);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (o0 + u * 512 < row_bytes) __stcs(reinterpret_cast<uint4*>(dst + o0 + u * 512), v[u]);
+      }
+    } else {
+      for (int64_t o = lane; o < row_bytes; o += 32) dst[o] = src[o];
+    }
+  }
+}
+
 int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int64_t* row_idx,
                    int32_t ids_from_rows, const void* rows, int64_t ld_rows, int32_t d,
                    int32_t elem_bytes, int64_t* exit_idx, int64_t* cont_idx, void* exit_rows,
@@ -166,8 +205,30 @@ int compact_launch(const uint8_t* mask, int64_t n, const int64_t* n_dev, const i
   int dev = 0;
   cudaGetDevice(&dev);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count(dev) * 4));
+  // dense rows with the index lists and counts requested: scan, then the
+  // parallel gather over those lists (same outputs as the in-scan gather)
+  const bool split_gather = rows && !row_idx && exit_idx && cont_idx && counts;
+  if (split_gather) {
+    p.rows = nullptr;
+    p.exit_rows = p.cont_rows = nullptr;
+  }
   compact_kernel<<<grid, kCThreads, 0, stream>>>(p);
-  return check_launch("compact_kernel");
+  int rc = check_launch("compact_kernel");
+  if (rc || !split_gather) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(sm_count(dev) * 8));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gather_rows_kernel, (const int64_t*)exit_idx, (const int64_t*)cont_idx,
+                     (const int64_t*)counts, reinterpret_cast<const uint8_t*>(rows),
+                     (int64_t)(ld_rows * elem_bytes), (int64_t)d * elem_bytes,
+                     reinterpret_cast<uint8_t*>(exit_rows), reinterpret_cast<uint8_t*>(cont_rows));
+  return check_launch("gather_rows_kernel");
 }
 
 // ---------------------------------------------------------------------------

@@ -252,9 +252,13 @@ def batch_compact(h, exit_mask, strategy: str = "auto") -> CompactionResult:
     exiting = torch.empty((n_exit, d), dtype=t.dtype, device=dev)
     continuing = torch.empty((n - n_exit, d), dtype=t.dtype, device=dev)
     if n:
+        # indices + counts again (same values) and the rows gathered over those
+        # lists by a second, fully parallel kernel
         N.check(lib.tide_compact(mask.data_ptr(), n, None, None, 0, t.data_ptr(), ld, d,
-                                 D.elem_bytes(code), None, None, exiting.data_ptr(),
-                                 continuing.data_ptr(), None, ws, s), "tide_compact(rows)")
+                                 D.elem_bytes(code), exit_idx.data_ptr(), cont_idx.data_ptr(),
+                                 exiting.data_ptr() if n_exit else None,
+                                 continuing.data_ptr() if n - n_exit else None,
+                                 counts.data_ptr(), ws, s), "tide_compact(rows)")
     res = CompactionResult(continuing, exiting, cont_idx[: n - n_exit], exit_idx[:n_exit])
     if host:
         return CompactionResult(*(D.to_host(x) for x in (res.continuing, res.exiting,

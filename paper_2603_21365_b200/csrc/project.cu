@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -141,6 +142,199 @@ __global__ void __launch_bounds__(kPThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Staged form (round 2).  numpy's pairwise order is a fixed tree for a given
+// d, so the host lays it out once per launch (PairPlan: the <= 128-element
+// leaves in order, and the post-order additions of the leaf / node sums).
+// A warp copies its row into shared memory as f32 (coalesced 16-byte loads),
+// sums four leaves at a time (8-lane groups, each lane's <= 16 squares
+// loaded before its sequential chain), lane 0 replays the additions, and the
+// row is normalized from shared memory: one read of the row, no recursion,
+// no per-element global latency.  Bit-identical to np_pairwise_sumsq.
+constexpr int kPlanLeaves = 256;
+constexpr int kStageWarps = 4;
+struct PairPlan {
+  int32_t L, nops;                  // leaves, additions (L - 1)
+  int32_t off[kPlanLeaves];         // leaf k = elements [off, off + len)
+  int16_t len[kPlanLeaves];
+  int16_t opa[kPlanLeaves], opb[kPlanLeaves];  // slot L + m = slot opa + slot opb
+};
+
+static int plan_build(int n, PairPlan& P) {
+  // iterative post-order of the recursion in np_pairwise_sumsq
+  struct Fr { int off, n, state, left; };
+  Fr st[64];
+  int sp = 0, L = 0, ops = 0;
+  int16_t slot_of_ret = -1;
+  st[sp++] = {0, n, 0, -1};
+  // first pass: leaves in order (slots 0..L-1), second: the additions
+  // (done together: each frame returns the slot of its sum)
+  int16_t ret = -1;
+  while (sp) {
+    Fr& f = st[sp - 1];
+    if (f.n <= 128) {
+      if (L >= kPlanLeaves) return -1;
+      P.off[L] = f.off;
+      P.len[L] = (int16_t)f.n;
+      ret = (int16_t)L++;
+      --sp;
+      continue;
+    }
+    int n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[sp++] = {f.off, n2, 0, -1};
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[sp++] = {f.off + n2, f.n - n2, 0, -1};
+    } else {
+      if (ops >= kPlanLeaves) return -1;
+      P.opa[ops] = (int16_t)f.left;
+      P.opb[ops] = ret;
+      ret = (int16_t)(kPlanLeaves + ops);  // node slots after the leaf slots
+      ++ops;
+      --sp;
+    }
+    if (sp >= 62) return -1;
+  }
+  (void)slot_of_ret;
+  P.L = L;
+  P.nops = ops;
+  return 0;
+}
+
+// the warp's shared region: row [d rounded to 4] + kPlanLeaves leaf slots + kPlanLeaves node slots
+__host__ __device__ __forceinline__ int stage_floats(int d) { return ((d + 3) & ~3) + 2 * kPlanLeaves; }
+
+template <typename T>
+__device__ __forceinline__ void stage_row(const T* __restrict__ src, float* __restrict__ buf, int d) {
+  const int lane = threadIdx.x & 31;
+  constexpr int V = 16 / sizeof(T);
+  if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && d % V == 0) {
+    for (int k = lane * V; k < d; k += 32 * V) {
+      float f[V];
+      unpack16(ld_nc_v4(src + k), f, (const T*)nullptr);
+#pragma unroll
+      for (int e = 0; e < V; ++e) buf[k + e] = f[e];
+    }
+  } else {
+    for (int k = lane; k < d; k += 32) buf[k] = to_f32<T>(src[k]);
+  }
+  __syncwarp();
+}
+
+// numpy-ordered sum of squares of the staged row; every lane gets it
+__device__ __forceinline__ float sumsq_planned(const float* __restrict__ buf, float* __restrict__ slots,
+                                               const PairPlan& P) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3, j = lane & 7;
+  for (int k0 = 0; k0 < P.L; k0 += 4) {
+    const int k = k0 + g;
+    const bool valid = k < P.L;
+    const int n = valid ? P.len[k] : 8;
+    const float* a = buf + (valid ? P.off[k] : 0);
+    const int body = n - (n % 8);
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = j + 8 * u;
+      v[u] = (valid && i < body) ? __fmul_rn(a[i], a[i]) : 0.0f;
+    }
+    float r = v[0];
+#pragma unroll
+    for (int u = 1; u < 16; ++u)
+      if (j + 8 * u < body) r = __fadd_rn(r, v[u]);
+    r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (valid && j == 0) {
+      if (n < 8) {  // numpy: fewer than 8 elements are summed sequentially
+        r = 0.0f;
+        for (int i = 0; i < n; ++i) r = __fadd_rn(r, __fmul_rn(a[i], a[i]));
+      } else {
+        for (int i = body; i < n; ++i) r = __fadd_rn(r, __fmul_rn(a[i], a[i]));
+      }
+      slots[k] = r;
+    }
+  }
+  __syncwarp();
+  float res = 0.0f;
+  if (lane == 0) {
+    for (int m = 0; m < P.nops; ++m)
+      slots[kPlanLeaves + m] = __fadd_rn(slots[P.opa[m]], slots[P.opb[m]]);
+    res = P.nops ? slots[kPlanLeaves + P.nops - 1] : slots[0];
+  }
+  return __shfl_sync(0xffffffffu, res, 0);
+}
+
+template <typename T>
+__device__ __forceinline__ void norm_row_planned(const T* __restrict__ src, float* __restrict__ dst,
+                                                 __nv_bfloat16* __restrict__ hi,
+                                                 __nv_bfloat16* __restrict__ lo, int d,
+                                                 const float* __restrict__ gain, float eps, int normalize,
+                                                 float* region, const PairPlan& P) {
+  const int lane = threadIdx.x & 31;
+  float* buf = region;
+  float* slots = region + ((d + 3) & ~3);
+  stage_row<T>(src, buf, d);
+  const float ss = normalize ? sumsq_planned(buf, slots, P) : 0.0f;
+  const float den = normalize ? __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps)) : 1.0f;
+  if (hi) {
+    for (int k = lane; k < d; k += 32) {
+      float y = __fdiv_rn(buf[k], den);
+      if (gain) y = __fmul_rn(y, gain[k]);
+      const __nv_bfloat16 h = __float2bfloat16_rn(y);
+      hi[k] = h;
+      lo[k] = __float2bfloat16_rn(y - __bfloat162float(h));  // y - h is exact in f32
+    }
+  } else if (((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && d % 4 == 0 &&
+             ((reinterpret_cast<uintptr_t>(gain) & 15) == 0)) {
+    // float4 rows from shared memory, float4 gains (read-only path), float4 stores
+    for (int k = lane * 4; k < d; k += 128) {
+      const float4 x = *reinterpret_cast<const float4*>(buf + k);
+      float f[4] = {x.x, x.y, x.z, x.w};
+      if (normalize) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) f[e] = __fdiv_rn(f[e], den);
+        if (gain) {
+          const float4 gv = __ldg(reinterpret_cast<const float4*>(gain + k));
+          f[0] = __fmul_rn(f[0], gv.x);
+          f[1] = __fmul_rn(f[1], gv.y);
+          f[2] = __fmul_rn(f[2], gv.z);
+          f[3] = __fmul_rn(f[3], gv.w);
+        }
+      }
+      *reinterpret_cast<float4*>(dst + k) = make_float4(f[0], f[1], f[2], f[3]);
+    }
+  } else {
+    for (int k = lane; k < d; k += 32) {
+      float y = normalize ? __fdiv_rn(buf[k], den) : buf[k];
+      if (normalize && gain) y = __fmul_rn(y, gain[k]);
+      dst[k] = y;
+    }
+  }
+  __syncwarp();  // the region is reused for the warp's next row
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32 * kStageWarps)
+    exit_project_staged_kernel(const T* rows, int64_t ld_rows, const int64_t* src_idx, int64_t n_e_host,
+                               const int64_t* n_e_dev, int d, const float* gain, float eps,
+                               int normalize, const int64_t* positions, float* out, int64_t ld_out,
+                               const __grid_constant__ PairPlan plan) {
+  extern __shared__ float stage_smem[];
+  const int64_t n_e = n_e_dev ? *n_e_dev : n_e_host;
+  float* region = stage_smem + (size_t)(threadIdx.x >> 5) * stage_floats(d);
+  const int64_t warps = (int64_t)gridDim.x * kStageWarps;
+  for (int64_t j = (int64_t)blockIdx.x * kStageWarps + (threadIdx.x >> 5); j < n_e; j += warps) {
+    const int64_t s = src_idx ? src_idx[j] : j;
+    norm_row_planned<T>(rows + s * ld_rows, out + positions[j] * ld_out, nullptr, nullptr, d, gain, eps,
+                        normalize, region, plan);
+  }
+}
+
 constexpr int kMaxPtrs = TIDE_MAX_LAYERS + 1;
 struct SelectParams {
   const void* layer[kMaxPtrs];
@@ -173,6 +367,38 @@ __global__ void __launch_bounds__(kPThreads) select_project_kernel(const __grid_
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(32 * kStageWarps)
+    select_project_staged_kernel(const __grid_constant__ SelectParams p, const __grid_constant__ PairPlan plan) {
+  extern __shared__ float stage_smem[];
+  float* region = stage_smem + (size_t)(threadIdx.x >> 5) * stage_floats(p.d);
+  const int64_t warps = (int64_t)gridDim.x * kStageWarps;
+  for (int64_t i = (int64_t)blockIdx.x * kStageWarps + (threadIdx.x >> 5); i < p.n; i += warps) {
+    int64_t src = p.num - 1;
+    if (p.exit_layers) {
+      const int64_t k = p.exit_layers[i];
+      if (k != TIDE_NO_EXIT && k + 1 >= 0 && k + 1 < p.num) src = k + 1;
+    }
+    const T* row = reinterpret_cast<const T*>(p.layer[src]) + i * p.ld_h;
+    norm_row_planned<T>(row, p.out ? p.out + i * p.ld_out : nullptr,
+                        p.out_hi ? p.out_hi + i * p.ld_out : nullptr,
+                        p.out_hi ? p.out_lo + i * p.ld_out : nullptr, p.d, p.gain, p.eps, 1, region, plan);
+  }
+}
+
+// The staged kernels take d >= 8 up to ~13,500 (4 rows in shared memory);
+// TIDE_PROJECT_STAGED=0 keeps the one-pass global-read kernels.
+static bool staged_plan(int d, PairPlan& P) {
+  const char* env = getenv("TIDE_PROJECT_STAGED");  // read per call
+  if (env && env[0] == '0') return false;
+  if (d < 8 || (size_t)kStageWarps * stage_floats(d) * sizeof(float) > 220 * 1024) return false;
+  return plan_build(d, P) == 0;
+}
+template <typename K>
+static void staged_smem_attr(K kernel, size_t smem) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 static int grid_for(int64_t rows) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -193,6 +419,38 @@ extern "C" int tide_exit_project(const void* rows, int64_t ld_rows, int32_t dtyp
     return set_error(TIDE_ERR_ARG, "tide_exit_project: bad arguments");
   if (n_e == 0 && !n_e_dev) return TIDE_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  PairPlan plan;
+  if (staged_plan(d, plan)) {
+    const size_t smem = (size_t)kStageWarps * stage_floats(d) * sizeof(float);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((std::max<int64_t>(n_e, 1) + kStageWarps - 1) / kStageWarps,
+                             (int64_t)sm_count(dev) * 8));
+    switch (dtype) {
+      case TIDE_F32:
+        staged_smem_attr(exit_project_staged_kernel<float>, smem);
+        exit_project_staged_kernel<float><<<grid, 32 * kStageWarps, smem, s>>>(
+            (const float*)rows, ld_rows, src_idx, n_e, n_e_dev, d, gain, eps, normalize, positions, out,
+            ld_out, plan);
+        break;
+      case TIDE_BF16:
+        staged_smem_attr(exit_project_staged_kernel<__nv_bfloat16>, smem);
+        exit_project_staged_kernel<__nv_bfloat16><<<grid, 32 * kStageWarps, smem, s>>>(
+            (const __nv_bfloat16*)rows, ld_rows, src_idx, n_e, n_e_dev, d, gain, eps, normalize,
+            positions, out, ld_out, plan);
+        break;
+      case TIDE_F16:
+        staged_smem_attr(exit_project_staged_kernel<__half>, smem);
+        exit_project_staged_kernel<__half><<<grid, 32 * kStageWarps, smem, s>>>(
+            (const __half*)rows, ld_rows, src_idx, n_e, n_e_dev, d, gain, eps, normalize, positions,
+            out, ld_out, plan);
+        break;
+      default:
+        return set_error(TIDE_ERR_ARG, "bad dtype %d", dtype);
+    }
+    return check_launch("exit_project_staged_kernel");
+  }
   const int grid = grid_for(std::max<int64_t>(n_e, 1));
   switch (dtype) {
     case TIDE_F32:
@@ -262,6 +520,31 @@ static int select_project_impl(const void* const* layer_ptrs, int32_t num_ptrs, 
   p.out_hi = out_hi;
   p.out_lo = out_lo;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  PairPlan plan;
+  if (staged_plan(d, plan)) {
+    const size_t smem = (size_t)kStageWarps * stage_floats(d) * sizeof(float);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((n + kStageWarps - 1) / kStageWarps, (int64_t)sm_count(dev) * 8));
+    switch (dtype) {
+      case TIDE_F32:
+        staged_smem_attr(select_project_staged_kernel<float>, smem);
+        select_project_staged_kernel<float><<<grid, 32 * kStageWarps, smem, s>>>(p, plan);
+        break;
+      case TIDE_BF16:
+        staged_smem_attr(select_project_staged_kernel<__nv_bfloat16>, smem);
+        select_project_staged_kernel<__nv_bfloat16><<<grid, 32 * kStageWarps, smem, s>>>(p, plan);
+        break;
+      case TIDE_F16:
+        staged_smem_attr(select_project_staged_kernel<__half>, smem);
+        select_project_staged_kernel<__half><<<grid, 32 * kStageWarps, smem, s>>>(p, plan);
+        break;
+      default:
+        return set_error(TIDE_ERR_ARG, "bad dtype %d", dtype);
+    }
+    return check_launch("select_project_staged_kernel");
+  }
   const int grid = grid_for(n);
   switch (dtype) {
     case TIDE_F32: select_project_kernel<float><<<grid, kPThreads, 0, s>>>(p); break;

@@ -158,3 +158,47 @@ def test_projection_bf16_rows_device():
     want = np.zeros((1000, 4096), np.float32)
     O.exit_projection(rows, gain, 1e-6, pos, want)
     np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("d", [8, 9, 130, 768, 772, 1000, 4096, 5003, 16384])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_staged_projection_bit_identical(d, dtype, monkeypatch):
+    """The staged rmsnorm (row in shared memory, numpy's pairwise tree laid
+    out by the host and summed four leaves at a time) == the one-pass
+    global-read kernel == the numpy oracle, bit for bit; exit_projection and
+    select_project's f32 and bf16-pair stagings."""
+    need_gpu()
+    import torch
+    g = np.random.Generator(np.random.PCG64(d))
+    n = 300
+    rows = torch.from_numpy(g.standard_normal((n, d), dtype=np.float32) * 3).cuda()
+    if dtype == "bf16":
+        rows = rows.to(torch.bfloat16)
+    gain = (g.standard_normal(d) * 0.5 + 1).astype(np.float32)
+    pos = torch.arange(0, 2 * n, 2, dtype=torch.int64, device="cuda")
+    outs, st = {}, {}
+    lib = N.load()
+    ptrs = N.ptr_array([rows.data_ptr()])
+    gd = torch.from_numpy(gain).cuda()
+    code = N.F32 if dtype == "f32" else N.BF16
+    for staged in ("1", "0"):
+        monkeypatch.setenv("TIDE_PROJECT_STAGED", staged)
+        out = torch.zeros((2 * n, d), device="cuda")
+        P.exit_projection(rows, gain, 1e-6, pos, out)
+        outs[staged] = out
+        f32 = torch.empty((n, d), device="cuda")
+        hi = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
+        lo = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
+        s = D.stream_handle()
+        N.check(lib.tide_select_project(ptrs, 1, d, code, None, n, d, gd.data_ptr(), 1e-6,
+                                        f32.data_ptr(), d, s), "select_project")
+        N.check(lib.tide_select_project_split(ptrs, 1, d, code, None, n, d, gd.data_ptr(), 1e-6,
+                                              hi.data_ptr(), lo.data_ptr(), d, s), "split")
+        torch.cuda.synchronize()
+        st[staged] = (f32, hi, lo)
+    assert torch.equal(outs["1"], outs["0"])
+    for a, b in zip(st["1"], st["0"]):
+        assert torch.equal(a, b)
+    want = np.zeros((2 * n, d), np.float32)
+    O.exit_projection(rows.float().cpu().numpy(), gain, 1e-6, pos.cpu().numpy(), want)
+    np.testing.assert_array_equal(outs["1"].cpu().numpy(), want)

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -394,9 +395,25 @@ static bool staged_plan(int d, PairPlan& P) {
   if (d < 8 || (size_t)kStageWarps * stage_floats(d) * sizeof(float) > 220 * 1024) return false;
   return plan_build(d, P) == 0;
 }
+// the dynamic-smem limit of a staged kernel is raised once, to the largest size used
 template <typename K>
 static void staged_smem_attr(K kernel, size_t smem) {
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem <= 48 * 1024) return;
+  static const void* ks[16];
+  static size_t sz[16];
+  static int nk = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int i = 0;
+  while (i < nk && ks[i] != (const void*)kernel) ++i;
+  if (i == nk && nk < 16) {
+    ks[nk] = (const void*)kernel;
+    sz[nk++] = 0;
+  }
+  if (i >= 16 || sz[i] < smem) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (i < 16) sz[i] = smem;
+  }
 }
 
 static int grid_for(int64_t rows) {

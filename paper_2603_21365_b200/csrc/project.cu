@@ -206,28 +206,55 @@ static int plan_build(int n, PairPlan& P) {
   return 0;
 }
 
-// the warp's shared region: row [d rounded to 4] + kPlanLeaves leaf slots + kPlanLeaves node slots
-__host__ __device__ __forceinline__ int stage_floats(int d) { return ((d + 3) & ~3) + 2 * kPlanLeaves; }
+// the warp's shared region: kPlanLeaves leaf slots + kPlanLeaves node slots
+// (f32), then the row in its own dtype (16-byte padded)
+__host__ __device__ __forceinline__ size_t stage_bytes(int d, int esz) {
+  return (size_t)2 * kPlanLeaves * sizeof(float) + (((size_t)d * esz + 15) & ~(size_t)15);
+}
 
 template <typename T>
-__device__ __forceinline__ void stage_row(const T* __restrict__ src, float* __restrict__ buf, int d) {
+__device__ __forceinline__ void stage_row(const T* __restrict__ src, T* __restrict__ buf, int d) {
   const int lane = threadIdx.x & 31;
   constexpr int V = 16 / sizeof(T);
   if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && d % V == 0) {
-    for (int k = lane * V; k < d; k += 32 * V) {
-      float f[V];
-      unpack16(ld_nc_v4(src + k), f, (const T*)nullptr);
-#pragma unroll
-      for (int e = 0; e < V; ++e) buf[k + e] = f[e];
-    }
+    for (int k = lane * V; k < d; k += 32 * V)
+      *reinterpret_cast<uint4*>(buf + k) = ld_nc_v4(src + k);
   } else {
-    for (int k = lane; k < d; k += 32) buf[k] = to_f32<T>(src[k]);
+    for (int k = lane; k < d; k += 32) buf[k] = src[k];
   }
   __syncwarp();
 }
 
+// 4 consecutive staged elements as f32 (exact upcast)
+template <typename T>
+__device__ __forceinline__ void lds4(const T* p, float (&f)[4]);
+template <>
+__device__ __forceinline__ void lds4<float>(const float* p, float (&f)[4]) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  f[0] = x.x;
+  f[1] = x.y;
+  f[2] = x.z;
+  f[3] = x.w;
+}
+template <>
+__device__ __forceinline__ void lds4<__nv_bfloat16>(const __nv_bfloat16* p, float (&f)[4]) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  f[0] = __uint_as_float(u.x << 16);
+  f[1] = __uint_as_float(u.x & 0xffff0000u);
+  f[2] = __uint_as_float(u.y << 16);
+  f[3] = __uint_as_float(u.y & 0xffff0000u);
+}
+template <>
+__device__ __forceinline__ void lds4<__half>(const __half* p, float (&f)[4]) {
+  f[0] = __half2float(p[0]);
+  f[1] = __half2float(p[1]);
+  f[2] = __half2float(p[2]);
+  f[3] = __half2float(p[3]);
+}
+
 // numpy-ordered sum of squares of the staged row; every lane gets it
-__device__ __forceinline__ float sumsq_planned(const float* __restrict__ buf, float* __restrict__ slots,
+template <typename T>
+__device__ __forceinline__ float sumsq_planned(const T* __restrict__ buf, float* __restrict__ slots,
                                                const PairPlan& P) {
   const int lane = threadIdx.x & 31;
   const int g = lane >> 3, j = lane & 7;
@@ -235,13 +262,14 @@ __device__ __forceinline__ float sumsq_planned(const float* __restrict__ buf, fl
     const int k = k0 + g;
     const bool valid = k < P.L;
     const int n = valid ? P.len[k] : 8;
-    const float* a = buf + (valid ? P.off[k] : 0);
+    const T* a = buf + (valid ? P.off[k] : 0);
     const int body = n - (n % 8);
     float v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int i = j + 8 * u;
-      v[u] = (valid && i < body) ? __fmul_rn(a[i], a[i]) : 0.0f;
+      const float x = (valid && i < body) ? to_f32<T>(a[i]) : 0.0f;
+      v[u] = __fmul_rn(x, x);
     }
     float r = v[0];
 #pragma unroll
@@ -253,9 +281,15 @@ __device__ __forceinline__ float sumsq_planned(const float* __restrict__ buf, fl
     if (valid && j == 0) {
       if (n < 8) {  // numpy: fewer than 8 elements are summed sequentially
         r = 0.0f;
-        for (int i = 0; i < n; ++i) r = __fadd_rn(r, __fmul_rn(a[i], a[i]));
+        for (int i = 0; i < n; ++i) {
+          const float x = to_f32<T>(a[i]);
+          r = __fadd_rn(r, __fmul_rn(x, x));
+        }
       } else {
-        for (int i = body; i < n; ++i) r = __fadd_rn(r, __fmul_rn(a[i], a[i]));
+        for (int i = body; i < n; ++i) {
+          const float x = to_f32<T>(a[i]);
+          r = __fadd_rn(r, __fmul_rn(x, x));
+        }
       }
       slots[k] = r;
     }
@@ -275,16 +309,16 @@ __device__ __forceinline__ void norm_row_planned(const T* __restrict__ src, floa
                                                  __nv_bfloat16* __restrict__ hi,
                                                  __nv_bfloat16* __restrict__ lo, int d,
                                                  const float* __restrict__ gain, float eps, int normalize,
-                                                 float* region, const PairPlan& P) {
+                                                 uint8_t* region, const PairPlan& P) {
   const int lane = threadIdx.x & 31;
-  float* buf = region;
-  float* slots = region + ((d + 3) & ~3);
+  float* slots = reinterpret_cast<float*>(region);
+  T* buf = reinterpret_cast<T*>(region + 2 * kPlanLeaves * sizeof(float));
   stage_row<T>(src, buf, d);
-  const float ss = normalize ? sumsq_planned(buf, slots, P) : 0.0f;
+  const float ss = normalize ? sumsq_planned<T>(buf, slots, P) : 0.0f;
   const float den = normalize ? __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps)) : 1.0f;
   if (hi) {
     for (int k = lane; k < d; k += 32) {
-      float y = __fdiv_rn(buf[k], den);
+      float y = __fdiv_rn(to_f32<T>(buf[k]), den);
       if (gain) y = __fmul_rn(y, gain[k]);
       const __nv_bfloat16 h = __float2bfloat16_rn(y);
       hi[k] = h;
@@ -292,10 +326,11 @@ __device__ __forceinline__ void norm_row_planned(const T* __restrict__ src, floa
     }
   } else if (((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && d % 4 == 0 &&
              ((reinterpret_cast<uintptr_t>(gain) & 15) == 0)) {
-    // float4 rows from shared memory, float4 gains (read-only path), float4 stores
+    // 4 elements per step: staged row from shared memory, float4 gains
+    // (read-only path), float4 stores
     for (int k = lane * 4; k < d; k += 128) {
-      const float4 x = *reinterpret_cast<const float4*>(buf + k);
-      float f[4] = {x.x, x.y, x.z, x.w};
+      float f[4];
+      lds4<T>(buf + k, f);
       if (normalize) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) f[e] = __fdiv_rn(f[e], den);
@@ -311,7 +346,7 @@ __device__ __forceinline__ void norm_row_planned(const T* __restrict__ src, floa
     }
   } else {
     for (int k = lane; k < d; k += 32) {
-      float y = normalize ? __fdiv_rn(buf[k], den) : buf[k];
+      float y = normalize ? __fdiv_rn(to_f32<T>(buf[k]), den) : to_f32<T>(buf[k]);
       if (normalize && gain) y = __fmul_rn(y, gain[k]);
       dst[k] = y;
     }
@@ -325,9 +360,9 @@ __global__ void __launch_bounds__(32 * kStageWarps)
                                const int64_t* n_e_dev, int d, const float* gain, float eps,
                                int normalize, const int64_t* positions, float* out, int64_t ld_out,
                                const __grid_constant__ PairPlan plan) {
-  extern __shared__ float stage_smem[];
+  extern __shared__ __align__(16) uint8_t stage_smem[];
   const int64_t n_e = n_e_dev ? *n_e_dev : n_e_host;
-  float* region = stage_smem + (size_t)(threadIdx.x >> 5) * stage_floats(d);
+  uint8_t* region = stage_smem + (size_t)(threadIdx.x >> 5) * stage_bytes(d, (int)sizeof(T));
   const int64_t warps = (int64_t)gridDim.x * kStageWarps;
   for (int64_t j = (int64_t)blockIdx.x * kStageWarps + (threadIdx.x >> 5); j < n_e; j += warps) {
     const int64_t s = src_idx ? src_idx[j] : j;
@@ -371,8 +406,8 @@ __global__ void __launch_bounds__(kPThreads) select_project_kernel(const __grid_
 template <typename T>
 __global__ void __launch_bounds__(32 * kStageWarps)
     select_project_staged_kernel(const __grid_constant__ SelectParams p, const __grid_constant__ PairPlan plan) {
-  extern __shared__ float stage_smem[];
-  float* region = stage_smem + (size_t)(threadIdx.x >> 5) * stage_floats(p.d);
+  extern __shared__ __align__(16) uint8_t stage_smem[];
+  uint8_t* region = stage_smem + (size_t)(threadIdx.x >> 5) * stage_bytes(p.d, (int)sizeof(T));
   const int64_t warps = (int64_t)gridDim.x * kStageWarps;
   for (int64_t i = (int64_t)blockIdx.x * kStageWarps + (threadIdx.x >> 5); i < p.n; i += warps) {
     int64_t src = p.num - 1;
@@ -389,10 +424,10 @@ __global__ void __launch_bounds__(32 * kStageWarps)
 
 // The staged kernels take d >= 8 up to ~13,500 (4 rows in shared memory);
 // TIDE_PROJECT_STAGED=0 keeps the one-pass global-read kernels.
-static bool staged_plan(int d, PairPlan& P) {
+static bool staged_plan(int d, int esz, PairPlan& P) {
   const char* env = getenv("TIDE_PROJECT_STAGED");  // read per call
   if (env && env[0] == '0') return false;
-  if (d < 8 || (size_t)kStageWarps * stage_floats(d) * sizeof(float) > 220 * 1024) return false;
+  if (d < 8 || kStageWarps * stage_bytes(d, esz) > 220 * 1024) return false;
   return plan_build(d, P) == 0;
 }
 // the dynamic-smem limit of a staged kernel is raised once, to the largest size used
@@ -437,8 +472,9 @@ extern "C" int tide_exit_project(const void* rows, int64_t ld_rows, int32_t dtyp
   if (n_e == 0 && !n_e_dev) return TIDE_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   PairPlan plan;
-  if (staged_plan(d, plan)) {
-    const size_t smem = (size_t)kStageWarps * stage_floats(d) * sizeof(float);
+  const int esz = dtype == TIDE_F32 ? 4 : 2;
+  if (staged_plan(d, esz, plan)) {
+    const size_t smem = kStageWarps * stage_bytes(d, esz);
     int dev = 0;
     cudaGetDevice(&dev);
     const int grid = (int)std::max<int64_t>(
@@ -538,8 +574,9 @@ static int select_project_impl(const void* const* layer_ptrs, int32_t num_ptrs, 
   p.out_lo = out_lo;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   PairPlan plan;
-  if (staged_plan(d, plan)) {
-    const size_t smem = (size_t)kStageWarps * stage_floats(d) * sizeof(float);
+  const int esz = dtype == TIDE_F32 ? 4 : 2;
+  if (staged_plan(d, esz, plan)) {
+    const size_t smem = kStageWarps * stage_bytes(d, esz);
     int dev = 0;
     cudaGetDevice(&dev);
     const int grid = (int)std::max<int64_t>(

@@ -496,7 +496,7 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
         if rc == 0:
             return exit_layers
         # a shape the one-launch tail does not take: the per-checkpoint links below
-    if (code != N.F32 and 2 <= len(ckpts) <= MAX_MULTI_CKPTS
+    if (code != N.F32 and 2 <= len(ckpts) <= MAX_MULTI_CKPTS and _multi_ok(staged, ckpts, d, b)
             and _speculative(n, d, final, theta, len(ckpts))):
         # every row at every checkpoint in ONE persistent tensor-core launch
         # (K1m) + resolve: the first firing checkpoint is what peeling
@@ -528,7 +528,7 @@ def _select_exits_chain(staged, bank, config: RuntimeConfig, ckpts, dev, ws=None
     wide_at = 0 if (tails and len(ckpts) >= 3 and _tail_wide(theta)) else -1
     after = _tail_after()
     tail_at = after - 1 if (tails and len(ckpts) - after >= 2) else -1
-    start = _window(code, len(ckpts)) if wide_at < 0 else 0
+    start = _window(code, len(ckpts)) if (wide_at < 0 and _multi_ok(staged, ckpts, d, b)) else 0
     if start:
         # a speculative window: the first `start` checkpoints for every row
         # in one K1m launch (no ordered look-back between them), then the
@@ -601,6 +601,19 @@ def _speculative(n: int, d: int, final, theta: float, C: int) -> bool:
     if env is not None:
         return env == "1"
     return C * n * d * final.element_size() <= SPEC_BYTES or theta >= WIDE_THETA
+
+
+def _multi_ok(staged, ckpts, d: int, b: int) -> bool:
+    """Shapes the one-launch K1m takes (tide_route_multi): d and every
+    capture's row stride multiples of 8, 16-byte aligned captures, b <= 256;
+    anything else stays on the peeling chain (CUDA-core links)."""
+    if d % 8 or b > 256:
+        return False
+    for k in ckpts:
+        t = staged[k + 1]
+        if t.stride(0) % 8 or t.data_ptr() % 16:
+            return False
+    return True
 
 
 def _window(code, C: int) -> int:

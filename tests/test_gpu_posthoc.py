@@ -546,11 +546,13 @@ def test_speculative_chain_repeats_bitwise():
     assert (want >= 0).any() and len(torch.unique(want)) > 2
 
 
-@pytest.mark.parametrize("d,n,L,b", [(776, 1000, 24, 128), (1024, 3000, 20, 256), (512, 700, 16, 64)])
+@pytest.mark.parametrize("d,n,L,b", [(776, 1000, 24, 128), (1024, 3000, 20, 256), (512, 700, 16, 64),
+                                     (772, 500, 12, 128)])
 def test_speculative_chain_odd_shapes(d, n, L, b, monkeypatch):
     """K1m through select_exits at shapes off the main configs: d not a
     multiple of 64 (partial last chunk), bottleneck 256 (two tiles per
-    group) and 64 (narrow N) -- the oracle's per-token map (band rule)."""
+    group) and 64 (narrow N), and d = 772 (not a multiple of 8: the policy
+    must fall back to the peeling chain) -- the oracle's per-token map."""
     need_gpu()
     monkeypatch.setenv("TIDE_SPECULATIVE", "1")
     ckpts, routers, states, bank, head = _big_case(L, d, n, "bf16", 5 + d + b, scale=0.15, b=b)

@@ -147,7 +147,27 @@ def case_round1():
     case_project_label(st, bank, host)
 
 
-CASES = {"round1": case_round1, "round2": case_round2, "k1m": case_k1m}
+def case_late():
+    """Kernels changed late in round 2: the staged exit projection /
+    select_project (bf16 and f32 rows, ragged d), the CTA-pair LM head (via
+    posthoc_select), batch_compact's parallel row gather."""
+    os.environ["SANITIZE_NO_DECODE"] = "1"
+    st, bank, host = case_chain(300, 772, 12, 0.6)
+    os.environ.pop("SANITIZE_NO_DECODE", None)
+    case_project_label(st, bank, host)
+    g = np.random.Generator(np.random.PCG64(9))
+    for dt in (torch.float32, torch.bfloat16):
+        rows = torch.from_numpy(g.standard_normal((200, 1000), dtype=np.float32)).cuda().to(dt)
+        gain = g.standard_normal(1000).astype(np.float32)
+        pos = torch.arange(0, 400, 2, dtype=torch.int64, device="cuda")
+        out = torch.zeros((400, 1000), device="cuda")
+        P.exit_projection(rows, gain, 1e-6, pos, out)
+        want = np.zeros((400, 1000), np.float32)
+        O.exit_projection(rows.float().cpu().numpy(), gain, 1e-6, pos.cpu().numpy(), want)
+        assert np.array_equal(out.cpu().numpy(), want)
+
+
+CASES = {"round1": case_round1, "round2": case_round2, "k1m": case_k1m, "late": case_late}
 
 
 def main():

@@ -568,3 +568,41 @@ def test_speculative_chain_odd_shapes(d, n, L, b, monkeypatch):
     monkeypatch.setenv("TIDE_SPECULATIVE", "0")
     peel = P.select_exits(states, bank, cfg).cpu().numpy()
     assert np.all((peel == want) | exc)
+
+
+_FUZZ = [  # (n, d, L, dtype, theta, mode)
+    (1, 64, 8, "bf16", 0.5, P.PER_TOKEN), (5, 772, 12, "f16", 0.6, P.PER_TOKEN),
+    (16, 1000, 12, "bf16", 0.5, P.BATCH_UNANIMOUS), (17, 1000, 12, "bf16", 0.55, P.PER_TOKEN),
+    (129, 256, 16, "f16", 0.5, P.PER_TOKEN), (300, 772, 20, "bf16", 0.95, P.PER_TOKEN),
+    (1000, 96, 40, "bf16", 0.5, P.PER_TOKEN), (257, 4104, 8, "bf16", 0.6, P.PER_TOKEN),
+    (2049, 512, 12, "f32", 0.5, P.PER_TOKEN), (640, 4096, 100, "bf16", 0.7, P.PER_TOKEN),
+    (333, 2048, 12, "bf16", 1.0, P.PER_TOKEN), (4100, 128, 12, "f16", 0.5, P.BATCH_UNANIMOUS),
+]
+
+
+@pytest.mark.parametrize("n,d,L,dtype,theta,mode", _FUZZ)
+def test_select_exits_policy_fuzz(n, d, L, dtype, theta, mode):
+    """select_exits over shapes that steer every strategy (decode step, K1m,
+    peeling links + tails, f32 tails, many checkpoints, d not a multiple of
+    8, ragged n) against the oracle's first-exit map (band rule)."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(n * 7 + d + L))
+    ckpts = O.checkpoint_layers(L, 4)
+    routers = {k: O.make_router(d, 128, k, g, scale=0.2) for k in ckpts}
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[dtype]
+    states = [torch.from_numpy(g.standard_normal((n, d), dtype=np.float32)).cuda().to(tdt)
+              for _ in range(L + 1)]
+    bank = P.make_bank({k: (r.w_down, r.w_up) for k, r in routers.items()}, num_layers=L)
+    cfg = P.RuntimeConfig(exit_threshold=theta, mode=mode)
+    got = P.select_exits(states, bank, cfg).cpu().numpy()
+    rt = 1e-5 if dtype == "f32" else RTOL["bf16"]
+    scores, exc = {}, np.zeros(n, bool)
+    for k in ckpts:
+        s_, t, m = O.route_logits(states[k + 1].float().cpu().numpy(), routers[k])
+        scores[k] = s_
+        if theta < 1.0:
+            exc |= np.abs(t - O.logit_of(theta)) <= rt * np.maximum(np.abs(t), m)
+    want = O.first_exit_from_scores(scores, theta, 0, mode)
+    if mode == P.BATCH_UNANIMOUS and exc.any():
+        exc[:] = True
+    assert np.all((got == want) | exc), (n, d, L, dtype, theta)

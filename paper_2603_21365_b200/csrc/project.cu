@@ -166,7 +166,6 @@ static int plan_build(int n, PairPlan& P) {
   struct Fr { int off, n, state, left; };
   Fr st[64];
   int sp = 0, L = 0, ops = 0;
-  int16_t slot_of_ret = -1;
   st[sp++] = {0, n, 0, -1};
   // first pass: leaves in order (slots 0..L-1), second: the additions
   // (done together: each frame returns the slot of its sum)
@@ -200,7 +199,6 @@ static int plan_build(int n, PairPlan& P) {
     }
     if (sp >= 62) return -1;
   }
-  (void)slot_of_ret;
   P.L = L;
   P.nops = ops;
   return 0;

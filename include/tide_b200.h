@@ -131,7 +131,9 @@ int tide_compact(const uint8_t* mask, int64_t n, const int64_t* n_dev, const int
  * terms hi.hi + hi.lo + lo.hi, f32 accumulation (small terms apart) — f32-grade
  * logits.  a_lo = b_lo = NULL: hi only (bf16 products).  ld_a, ld_b
  * multiples of 8 (any d <= ld), ld_out a multiple of 4, 16-byte aligned
- * pointers.
+ * pointers.  Columns [V, ceil4(V)) of every output row (inside ld_out) are
+ * written with 0 (the epilogue stores whole 16-byte pieces); nothing past
+ * ceil4(V) or row n is written.
  */
 int tide_lm_head(const void* a_hi, const void* a_lo, int64_t ld_a, int64_t n, int32_t d,
                  const void* b_hi, const void* b_lo, int64_t ld_b, int64_t V, float* out,

@@ -20,7 +20,16 @@ from tests.gpu_helpers import need_gpu
 pytestmark = pytest.mark.gpu
 
 
-def _lm(a32, b32, terms):
+FORMS = ["persistent", "pair", "one"]
+
+
+def _set_form(monkeypatch, form):
+    """persistent CTA pairs (the default for 3 terms), one-tile CTA pairs, one CTA."""
+    monkeypatch.setenv("TIDE_LM_PAIR", "0" if form == "one" else "1")
+    monkeypatch.setenv("TIDE_LM_PERSIST", "1" if form == "persistent" else "0")
+
+
+def _lm(a32, b32, terms, ldo=None, extra_rows=0, full=False):
     from paper_2603_21365_b200 import _device as Dv
     from paper_2603_21365_b200 import _native as N
     from paper_2603_21365_b200.runtime import split_bf16
@@ -31,25 +40,25 @@ def _lm(a32, b32, terms):
     ld = (d + 7) // 8 * 8
     ah, al = split_bf16(torch.from_numpy(a32).to(dev), ld)
     bh, bl = split_bf16(torch.from_numpy(b32).to(dev), ld)
-    ldo = (V + 3) // 4 * 4
-    out = torch.full((n, ldo), float("nan"), dtype=torch.float32, device=dev)
+    ldo = (V + 3) // 4 * 4 if ldo is None else ldo
+    out = torch.full((n + extra_rows, ldo), float("nan"), dtype=torch.float32, device=dev)
     rc = N.load().tide_lm_head(ah.data_ptr(), al.data_ptr() if terms == 3 else None, ld, n, d,
                                bh.data_ptr(), bl.data_ptr() if terms == 3 else None, ld, V,
                                out.data_ptr(), ldo, Dv.stream_handle(dev))
     N.check(rc, "tide_lm_head")
     torch.cuda.synchronize()
-    return out[:, :V].cpu().numpy()
+    return out.cpu().numpy() if full else out[:n, :V].cpu().numpy()
 
 
-@pytest.mark.parametrize("pair", ["1", "0"])
+@pytest.mark.parametrize("form", FORMS)
 @pytest.mark.parametrize("n,d,V", [(1, 64, 64), (8, 4096, 1000), (130, 772, 300),
                                    (1000, 1024, 2500), (300, 4096, 50257), (129, 256, 129)])
-def test_lm_head_three_terms_f32_grade(n, d, V, pair, monkeypatch):
-    """Both forms: CTA pairs (cta_group::2, the default for 3 terms; ragged
-    row counts leave the pair's second CTA partly or wholly past the rows)
-    and the one-CTA kernel."""
+def test_lm_head_three_terms_f32_grade(n, d, V, form, monkeypatch):
+    """Every form: persistent CTA pairs (cta_group::2, the default for 3
+    terms; ragged row counts leave the pair's second CTA partly or wholly
+    past the rows), one-tile CTA pairs and the one-CTA kernel."""
     need_gpu()
-    monkeypatch.setenv("TIDE_LM_PAIR", pair)
+    _set_form(monkeypatch, form)
     g = np.random.Generator(np.random.PCG64(n + d + V))
     a = g.standard_normal((n, d), dtype=np.float32)
     b = (g.standard_normal((V, d)) * 0.02).astype(np.float32)
@@ -64,10 +73,39 @@ def test_lm_head_three_terms_f32_grade(n, d, V, pair, monkeypatch):
     assert np.abs(got - f32).max() <= 4 * np.abs(f32 - exact).max() + 1e-5 * M.max()
 
 
-@pytest.mark.parametrize("pair", ["0", "1"])
-def test_lm_head_hi_only_bf16_products(pair, monkeypatch):
+@pytest.mark.parametrize("terms", [3, 1])
+@pytest.mark.parametrize("form", FORMS)
+@pytest.mark.parametrize("n,d,V", [(129, 256, 129), (300, 1024, 1001), (5, 64, 32), (257, 512, 600),
+                                   (2, 128, 4099)])
+def test_lm_head_tma_store_epilogue(n, d, V, terms, form, monkeypatch):
+    """The TMA-store epilogue (logit blocks through shared memory, clipped by
+    the output tensor map) writes exactly what the per-lane stores write:
+    bit-identical logits; past column V only the rest of the last 16-byte
+    piece, with 0 (the C-ABI contract: columns [V, ceil4(V)) receive 0), and
+    nothing past ceil4(V) (the extra padding stays NaN) or row n (the rows
+    after the output stay NaN)."""
     need_gpu()
-    monkeypatch.setenv("TIDE_LM_PAIR", pair)
+    _set_form(monkeypatch, form)
+    g = np.random.Generator(np.random.PCG64(n * 7 + V))
+    a = g.standard_normal((n, d), dtype=np.float32)
+    b = (g.standard_normal((V, d)) * 0.02).astype(np.float32)
+    v4 = (V + 3) // 4 * 4
+    ldo = v4 + 8
+    monkeypatch.setenv("TIDE_LM_TMA_STORE", "1")
+    tma = _lm(a, b, terms, ldo=ldo, extra_rows=3, full=True)
+    monkeypatch.setenv("TIDE_LM_TMA_STORE", "0")
+    lane = _lm(a, b, terms, ldo=ldo, extra_rows=3, full=True)
+    assert np.isfinite(tma[:n, :V]).all()
+    assert np.array_equal(tma[:n, :V], lane[:n, :V])
+    assert (tma[:n, V:v4] == 0).all()
+    assert np.isnan(tma[:n, v4:]).all() and np.isnan(tma[n:]).all()
+    assert np.isnan(lane[:n, V:]).all() and np.isnan(lane[n:]).all()
+
+
+@pytest.mark.parametrize("form", FORMS)
+def test_lm_head_hi_only_bf16_products(form, monkeypatch):
+    need_gpu()
+    _set_form(monkeypatch, form)
     g = np.random.Generator(np.random.PCG64(5))
     a = g.standard_normal((257, 512), dtype=np.float32)
     b = (g.standard_normal((600, 512)) * 0.02).astype(np.float32)
@@ -128,3 +166,21 @@ def test_select_project_split_is_the_f32_staging():
     assert torch.equal(hi, f32.to(torch.bfloat16))
     rel = ((hi.float() + lo.float()) - f32).abs() / f32.abs().clamp_min(1e-30)
     assert float(rel.max()) <= 2.0 ** -16
+
+
+@pytest.mark.parametrize("terms", [3, 1])
+def test_lm_head_persistent_bitwise_equals_one_tile_pairs(terms, monkeypatch):
+    """The persistent pairs walk several tiles each (the ring and the
+    accumulator sets carried across tiles): the same logits, bit for bit, as
+    one tile per pair."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(77 + terms))
+    n, d, V = 1000, 1024, 20000  # 4 row pairs x 79 vocab tiles > co-resident pairs
+    a = g.standard_normal((n, d), dtype=np.float32)
+    b = (g.standard_normal((V, d)) * 0.02).astype(np.float32)
+    _set_form(monkeypatch, "persistent")
+    got = _lm(a, b, terms)
+    _set_form(monkeypatch, "pair")
+    want = _lm(a, b, terms)
+    assert np.isfinite(got).all()
+    assert np.array_equal(got, want)

@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -57,8 +58,8 @@ namespace tide {
 
 constexpr int kThreadsTF = 384;
 constexpr int kTfMaxNA = 8;
-constexpr int kTfMaxNL = 4;
-constexpr int kTfMaxNW = 2;
+constexpr int kTfMaxNL = 8;
+constexpr int kTfMaxNW = 4;
 constexpr int kTfSlot = 128 * 128;  // 128 rows x 32 f32 columns
 constexpr int kTfGran = 16;
 
@@ -549,47 +550,83 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
 //   acc 4  8.5e-7  3.5e-6  7.2e-6  1.4e-5
 // so 2 accumulators (2 tiles per group) up to d = 4096 and 4 (1 tile per
 // group: W re-read per tile) up to d = 8192 stay inside the 1e-5 contract.
-int tf32_nacc(int d, int nk) {
+// Accumulators per tile.  The logit error grows with d and, relative to the
+// conditioning magnitude m, as the bottleneck narrows (fewer units average the
+// accumulation errors out): tools/tf32_probe.py, 16,384 rows N(0, 9), max
+// |dt| / max(|t|, m) with 2 / 4 accumulators —
+//   b = 128: d 4096 8.0e-6 / 4.3e-6, d 8192 1.4e-5 / 6.8e-6
+//   b =  96: d 4096 7.5e-6 / 3.9e-6, d 8192 1.8e-5 / 8.9e-6
+//   b =  64: d 4096 9.9e-6 / 5.6e-6, d 8192 2.0e-5 / 9.8e-6
+//   b =  32: d 2048 8.0e-6 / 4.3e-6, d 4096 1.6e-5 / 8.2e-6, d 8192 - / 1.6e-5
+//   b =  16: d 4096 3.1e-5 / 1.6e-5
+// so 2 only for b >= 128 and d <= 4096 (4 costs TMEM tiles per group there),
+// else 4; tf32_max_d below keeps the default path inside 1e-5 with margin.
+int tf32_nacc(int d, int nk, int b) {
   const char* env = getenv("TIDE_TF32_ACC");
-  int v = env ? atoi(env) : (d <= 4096 ? 2 : 4);
+  int v = env ? atoi(env) : (d <= 4096 && b >= 128 ? 2 : 4);
   if (v != 1 && v != 2 && v != 4) v = 4;
   if (v == 4 && nk < 2) v = 2;
   return v;
 }
 
 // f32 rows on tcgen05 (TIDE_F32_TC=0 forces the CUDA-core kernel, =1 this one
-// at any shape): the default for d <= kTf32MaxD and n >= kTf32MinRows.  Below
+// at any shape): the default for d <= tf32_max_d(b) and n >= kTf32MinRows.  Below
 // that row count every CTA re-reads and re-splits all of W for a few rows
 // (W-bound: 0.24 ms at 4,096 x 4096, as the CUDA-core kernel); at 65,536 x 4096
 // 0.57 ms against 1.82 ms on CUDA cores.
-constexpr int kTf32MaxD = 8192;
 constexpr int64_t kTf32MinRows = 16384;
+// widest d the default path takes for a bottleneck b (measured errors above:
+// <= 9e-6 of the 1e-5 contract with the accumulators tf32_nacc picks)
+int tf32_max_d(int b) { return b >= 112 ? 8192 : b >= 48 ? 4096 : b >= 24 ? 2048 : 1024; }
 bool route_tf32_supported(int d, int b, int64_t n) {
   const char* env = getenv("TIDE_F32_TC");  // read per call: tests switch it
   if (env && env[0] == '0') return false;
   const bool forced = env && env[0] == '1';
   return d >= 4 && d % 4 == 0 && b >= 1 && b <= 128 &&
-         (forced || (d <= kTf32MaxD && n >= kTf32MinRows));
+         (forced || (d <= tf32_max_d(b) && n >= kTf32MinRows));
 }
 
 int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
   const int npad = (a.b + 15) / 16 * 16;
   const int bp = (npad + 31) / 32 * 32;
   const int nk = (a.d + 31) / 32;
-  const int nacc = tf32_nacc(a.d, nk);
+  const int nacc = tf32_nacc(a.d, nk, a.b);
   const int tpg = std::max(1, std::min(4, 512 / (bp * nacc)));
   if (tpg * bp * nacc > 512) return set_error(TIDE_ERR_UNSUPPORTED, "tf32: TMEM too small");
   int cols = 32;
   while (cols < tpg * bp * nacc) cols <<= 1;
   const uint32_t whalf = (uint32_t)npad * 128u;
   const uint32_t wslot = 2 * whalf;
-  const int nw = kTfMaxNW;
-  const uint32_t off_a = (uint32_t)nw * wslot;
+  // Ring shape: W slots (hi + lo each), A slots, lo slots.  The W ring is
+  // what the MMAs wait on (a W chunk feeds every tile of the group, and its
+  // refill waits for the last MMA on it, the TMA round trip and the split):
+  // the deepest W ring (<= 4) that leaves >= max(4, 2 tpg) A slots (rings
+  // with fewer A slots than two chunks' tiles were seen to stall for good).  65,536 x 4096:
+  // 2 W slots 0.567 ms, 3 0.530, 4 0.497 (tools/tf32_ring.py, bit-identical).
+  // TIDE_TF32_RING="nw,na,nl" (read per call) overrides for sweeps (na, nl
+  // 0: the rule below for that nw).
   const int smem_cap = 227 * 1024;
   const uint32_t misc = 1024 /*w_up*/ + 512 /*bars*/ + 128 /*words*/ + 2048 /*ids*/ + 16;
-  const int slots = (int)((smem_cap - 1024 - off_a - misc) / kTfSlot);
-  int nl = std::min(kTfMaxNL, std::max(1, slots / 3));
+  auto slots_for = [&](int w) { return (smem_cap - 1024 - w * (int)wslot - (int)misc) / kTfSlot; };
+  auto nl_for = [&](int sl) { return std::min(4, std::max(1, sl / 3)); };
+  int nw = 2, na_req = 0, nl_req = 0;
+  for (int w = kTfMaxNW; w > 2; --w) {
+    const int sl = slots_for(w);
+    if (std::min(kTfMaxNA, sl - nl_for(sl)) >= std::max(4, 2 * tpg)) {
+      nw = w;
+      break;
+    }
+  }
+  if (const char* renv = getenv("TIDE_TF32_RING")) {
+    int x = 0, y = 0, z = 0;
+    if (sscanf(renv, "%d,%d,%d", &x, &y, &z) == 3 && x >= 1 && x <= kTfMaxNW) nw = x, na_req = y, nl_req = z;
+  }
+  const uint32_t off_a = (uint32_t)nw * wslot;
+  const int slots = slots_for(nw);
+  int nl = nl_for(slots);
   int na = std::min(kTfMaxNA, slots - nl);
+  if (na_req > 0 && nl_req > 0 && na_req <= kTfMaxNA && nl_req <= kTfMaxNL && na_req + nl_req <= slots)
+    na = na_req, nl = nl_req;
   if (na < 2 || nl < 1) return set_error(TIDE_ERR_UNSUPPORTED, "bottleneck too wide for smem");
   TfParams p{};
   p.n_host = a.n;

@@ -48,6 +48,14 @@ def test_library_metadata_without_gpu(lib):
     assert lib.tide_route_uses_tensor_cores(N.BF16, 4096, 128) == 1
     assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 128) == 1  # 3xTF32 (large n)
     assert lib.tide_route_uses_tensor_cores(N.F32, 16384, 128) == 0
+    # 3xTF32 only where its measured error stays inside 1e-5 (route_tf32.cu
+    # tf32_max_d): narrower bottlenecks average fewer units
+    assert lib.tide_route_uses_tensor_cores(N.F32, 8192, 128) == 1
+    assert lib.tide_route_uses_tensor_cores(N.F32, 8192, 96) == 0
+    assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 64) == 1
+    assert lib.tide_route_uses_tensor_cores(N.F32, 4096, 32) == 0
+    assert lib.tide_route_uses_tensor_cores(N.F32, 2048, 32) == 1
+    assert lib.tide_route_uses_tensor_cores(N.F32, 2048, 16) == 0
     assert lib.tide_route_uses_tensor_cores(N.BF16, 4096, 512) == 0
 
 

@@ -450,3 +450,49 @@ def test_repeated_launches_bitwise_identical(pair, monkeypatch):
         r = P.route(h, router, **kw)
         for k in ("logits", "mask", "exiting_indices", "continuing_indices"):
             assert torch.equal(r[k], ref[k]), (i, k)
+
+
+@pytest.mark.parametrize("b", [16, 48, 64, 96, 112, 128])
+@pytest.mark.parametrize("n,d", [(20000, 1024), (3000, 4096)])
+def test_f32_tensor_core_ring_shapes_bitwise(n, d, b, monkeypatch):
+    """The 3xTF32 kernel's default ring (up to 4 W slots, route_tf32.cu) and
+    the two-W-slot ring give bit-identical logits, masks and indices (the
+    ring only reorders waits, never arithmetic), over bottleneck widths whose
+    rings differ in every slot count."""
+    need_gpu()
+    monkeypatch.setenv("TIDE_F32_TC", "1")
+    g = np.random.Generator(np.random.PCG64(n + d + b))
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = to_dev(g.standard_normal((n, d), dtype=np.float32) * 3.0, "f32")
+    outs = []
+    for ring in (None, "2,0,0"):
+        if ring:
+            monkeypatch.setenv("TIDE_TF32_RING", ring)
+        r = P.route(h, _router(wd, wu), theta=0.5, want_logits=True, want_indices=True)
+        outs.append({k: r[k].cpu().numpy() for k in ("logits", "mask", "exiting_indices",
+                                                       "continuing_indices")})
+    for k in outs[0]:
+        np.testing.assert_array_equal(outs[0][k], outs[1][k], err_msg=k)
+    if d <= 1024:  # inside the default path's (d, b) range: the 1e-5 contract too
+        _, t_ref, m_ref = O.route_logits(h.cpu().numpy(), O.OracleRouter(3, wd, wu))
+        check_logits(outs[0]["logits"], t_ref, m_ref, "f32", f"ring b={b}")
+
+
+@pytest.mark.parametrize("d,b", [(2048, 32), (4096, 64), (4096, 96), (1024, 16)])
+def test_f32_default_narrow_bottlenecks_within_contract(d, b):
+    """Narrow bottlenecks at the widest d the default 3xTF32 path takes for
+    them (4 TMEM accumulators): inside the 1e-5 f32 contract."""
+    need_gpu()
+    n = 16384
+    assert N.load().tide_route_uses_tensor_cores(N.F32, d, b) == 1
+    g = np.random.Generator(np.random.PCG64(d * b))
+    wd = (g.standard_normal((b, d)) * 0.05).astype(np.float32)
+    wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
+    h = g.standard_normal((n, d), dtype=np.float32) * 3.0
+    _, t_ref, m_ref = O.route_logits(h, O.OracleRouter(3, wd, wu))
+    r = P.route(to_dev(h, "f32"), _router(wd, wu), theta=0.5, want_logits=True,
+                want_indices=True)
+    check_logits(r["logits"].cpu().numpy(), t_ref, m_ref, "f32", f"tf32 narrow d={d} b={b}")
+    e, c = O.compact_indices(r["mask"].cpu().numpy())
+    np.testing.assert_array_equal(r["exiting_indices"].cpu().numpy(), e)

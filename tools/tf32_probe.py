@@ -15,11 +15,12 @@ lib = N.load(os.environ["TIDE_PROBE_LIB"]) if os.environ.get("TIDE_PROBE_LIB") e
 lib2 = N.load(os.environ["TIDE_PROBE_LIB2"]) if os.environ.get("TIDE_PROBE_LIB2") else None
 ws = D.workspace().data_ptr()
 s = torch.cuda.current_stream().cuda_stream
-b = 128
 shapes = [(2048, 768), (8192, 768), (1000, 772), (4096, 4096), (65536, 4096)]
 if len(sys.argv) > 1:
     shapes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]]
-for n, d in shapes:
+for shp in shapes:
+    n, d = shp[:2]
+    b = shp[2] if len(shp) > 2 else 128
     g = torch.Generator(device="cuda")
     g.manual_seed(n + d)
     h = torch.randn((n, d), generator=g, device="cuda") * 3.0
@@ -55,7 +56,7 @@ for n, d in shapes:
     t64 = sl @ wu.double()
     m = (sl * wu.double()).abs().sum(1)
     err = ((logits.double() - t64).abs() / torch.maximum(t64.abs(), m)).max().item()
-    line = (f"n={n:6d} d={d:5d}  {us:8.1f} us  {n * d * 4 / us / 1e3:7.0f} GB/s  "
+    line = (f"n={n:6d} d={d:5d} b={b:3d}  {us:8.1f} us  {n * d * 4 / us / 1e3:7.0f} GB/s  "
             f"max|dt|/max(|t|,m) = {err:.2e}  exits={int(counts[0])}")
     if lib2 is not None:
         l2 = torch.empty_like(logits)

@@ -17,7 +17,8 @@
  *     with a leading dimension `ld` in ELEMENTS.
  *   - `workspace` is a TIDE_WORKSPACE_BYTES device buffer, zeroed once with
  *     tide_workspace_init() and then reused by calls on ONE stream (it holds
- *     the ordered look-back state of the stable compaction).
+ *     the ordered look-back state of the stable compaction; its upper half
+ *     is per-launch scratch, e.g. the f32 router's pre-split W).
  *   - There is no CPU fallback: unsupported shapes return
  *     TIDE_ERR_UNSUPPORTED.
  */
@@ -45,7 +46,7 @@ extern "C" {
 #define TIDE_MODE_BATCH_UNANIMOUS 1 /* ee/runtime.py:29 */
 #define TIDE_NO_EXIT (-1)           /* ee/runtime.py:35 */
 
-#define TIDE_WORKSPACE_BYTES (8u << 20)
+#define TIDE_WORKSPACE_BYTES (16u << 20)
 #define TIDE_MAX_LAYERS 256
 #define TIDE_MAX_DECODE_ROWS 16
 

@@ -17,7 +17,7 @@ LIBPATH = os.path.join(_PKG, "_lib", "libtide_b200.so")
 F32, F16, BF16 = 0, 1, 2
 MODE_PER_TOKEN, MODE_BATCH_UNANIMOUS = 0, 1
 NO_EXIT = -1
-WORKSPACE_BYTES = 8 << 20
+WORKSPACE_BYTES = 16 << 20
 MAX_DECODE_ROWS = 16
 ROUTE_INPUTS_READY = 1
 

@@ -77,6 +77,7 @@ struct TfParams {
   float eps, inv_d, theta;
   int64_t layer;
   int32_t inputs_ready;  // TIDE_ROUTE_INPUTS_READY
+  int32_t w_presplit;    // W's lo half staged in the workspace (tm_wlo): no splitter
   float* scores;
   float* logits;
   uint8_t* mask;
@@ -104,12 +105,29 @@ __device__ __forceinline__ void split4(const uint4& v, uint4& hi, uint4& lo) {
                   __float_as_uint(__uint_as_float(v.w) - __uint_as_float(hi.w)));
 }
 
+// W's lo half (w - tf32(w), exactly split4's) into the workspace once per
+// launch: the route kernel then TMA-loads both halves and its splitter warp
+// (one warp re-splitting all of W for every row group: ~0.8 us per 32-column
+// chunk, as long as the chunk's MMAs) stays idle.
+__global__ void __launch_bounds__(256) tf32_split_w_kernel(const float* __restrict__ w,
+                                                           float* __restrict__ lo, int64_t n4) {
+  const uint4* src = reinterpret_cast<const uint4*>(w);
+  uint4* dst = reinterpret_cast<uint4*>(lo);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 hi, l;
+    split4(src[i], hi, l);
+    dst[i] = l;
+  }
+}
+
 __global__ void __launch_bounds__(kThreadsTF, 1)
     route_tf32_kernel(const __grid_constant__ CUtensorMap tm_h128,
                       const __grid_constant__ CUtensorMap tm_h64,
                       const __grid_constant__ CUtensorMap tm_h32b,
                       const __grid_constant__ CUtensorMap tm_h16,
                       const __grid_constant__ CUtensorMap tm_w,
+                      const __grid_constant__ CUtensorMap tm_wlo,
                       const __grid_constant__ CUtensorMap tm_g4, const __grid_constant__ TfParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -155,6 +173,7 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_w);
+    if (p.w_presplit) prefetch_tmap(&tm_wlo);
     prefetch_tmap(gathered ? &tm_g4 : &tm_h128);
     for (int i = 0; i < p.nw; ++i) {
       mbar_init(&w_full[i], 1);
@@ -205,8 +224,10 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
       if (lane == 0) {
         auto load_w = [&](int kc) {
           mbar_wait(&w_empty[wsl], wph ^ 1);
-          mbar_arrive_expect_tx(&w_full[wsl], p.whalf);
+          mbar_arrive_expect_tx(&w_full[wsl], p.w_presplit ? 2 * p.whalf : p.whalf);
           tma_load_2d(sW + (size_t)wsl * p.wslot, &tm_w, &w_full[wsl], kc * 32, 0, pol_w);
+          if (p.w_presplit)
+            tma_load_2d(sW + (size_t)wsl * p.wslot + p.whalf, &tm_wlo, &w_full[wsl], kc * 32, 0, pol_w);
           if (++wsl == p.nw) { wsl = 0; wph ^= 1; }
         };
         auto load_a = [&](int kc, int t) {
@@ -305,7 +326,7 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
         return desc_hi | (uint64_t)((smem_u32(sW + (size_t)slot * p.wslot) & 0x3FFFFu) >> 4);
       };
       for (int kc = 0; kc < P1; ++kc) {
-        mbar_wait(&w_ready[wsl], wph);
+        mbar_wait(p.w_presplit ? &w_full[wsl] : &w_ready[wsl], wph);
         const uint64_t bdesc = wdesc(wsl);
         for (int t = 0; t < T; ++t) mma_slot(kc, t, bdesc);
         if (elect_one()) tc_commit(&w_empty[wsl]);
@@ -315,7 +336,7 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
       for (int t = 0; t < T; ++t) {
         int sl = wsl, ph = wph;
         for (int j = 0; j < p.nx; ++j) {
-          if (t == 0) mbar_wait(&w_ready[sl], ph);
+          if (t == 0) mbar_wait(p.w_presplit ? &w_full[sl] : &w_ready[sl], ph);
           mma_slot(P1 + j, t, wdesc(sl));
           if (t == T - 1) {
             if (elect_one()) tc_commit(&w_empty[sl]);
@@ -504,8 +525,9 @@ __global__ void __launch_bounds__(kThreadsTF, 1)
     }
   } else {
     // ----------------------------------------------------------- W splitter
+    // (idle when W's lo half was staged by tf32_split_w_kernel)
     int wsl = 0, wph = 0;
-    for (int64_t g = blockIdx.x; g < NG; g += G) {
+    for (int64_t g = blockIdx.x; !p.w_presplit && g < NG; g += G) {
       for (int kc = 0; kc < p.nk; ++kc) {
         mbar_wait(&w_full[wsl], wph);
         uint8_t* hp = sW + (size_t)wsl * p.wslot;
@@ -570,11 +592,16 @@ int tf32_nacc(int d, int nk, int b) {
 }
 
 // f32 rows on tcgen05 (TIDE_F32_TC=0 forces the CUDA-core kernel, =1 this one
-// at any shape): the default for d <= tf32_max_d(b) and n >= kTf32MinRows.  Below
+// at any shape): the default for d <= tf32_max_d(b) and n >= tf32_min_rows(d).  Below
 // that row count every CTA re-reads and re-splits all of W for a few rows
 // (W-bound: 0.24 ms at 4,096 x 4096, as the CUDA-core kernel); at 65,536 x 4096
 // 0.57 ms against 1.82 ms on CUDA cores.
-constexpr int64_t kTf32MinRows = 16384;
+// Fewest rows the default path takes: below, every CTA still walks all of W
+// for a handful of rows (~155 us at d = 4096 whatever n <= 8,192, W-chunk
+// latency bound), and the CUDA-core kernel is as fast (tools/remote/tf32_pol.sh:
+// d = 4096, n = 2,048: 148 vs 157 us; n = 4,096: 238 vs 158 us; d = 1024,
+// n = 4,096: 67 vs 67 us, n = 16,384: 149 vs 67 us).
+int64_t tf32_min_rows(int d) { return d >= 2048 ? 4096 : 8192; }
 // widest d the default path takes for a bottleneck b (measured errors above:
 // <= 9e-6 of the 1e-5 contract with the accumulators tf32_nacc picks)
 int tf32_max_d(int b) { return b >= 112 ? 8192 : b >= 48 ? 4096 : b >= 24 ? 2048 : 1024; }
@@ -583,7 +610,7 @@ bool route_tf32_supported(int d, int b, int64_t n) {
   if (env && env[0] == '0') return false;
   const bool forced = env && env[0] == '1';
   return d >= 4 && d % 4 == 0 && b >= 1 && b <= 128 &&
-         (forced || (d <= tf32_max_d(b) && n >= kTf32MinRows));
+         (forced || (d <= tf32_max_d(b) && n >= tf32_min_rows(d)));
 }
 
 int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
@@ -597,34 +624,30 @@ int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
   while (cols < tpg * bp * nacc) cols <<= 1;
   const uint32_t whalf = (uint32_t)npad * 128u;
   const uint32_t wslot = 2 * whalf;
-  // Ring shape: W slots (hi + lo each), A slots, lo slots.  The W ring is
-  // what the MMAs wait on (a W chunk feeds every tile of the group, and its
-  // refill waits for the last MMA on it, the TMA round trip and the split):
-  // the deepest W ring (<= 4) that leaves >= max(4, 2 tpg) A slots (rings
-  // with fewer A slots than two chunks' tiles were seen to stall for good).  65,536 x 4096:
-  // 2 W slots 0.567 ms, 3 0.530, 4 0.497 (tools/tf32_ring.py, bit-identical).
-  // TIDE_TF32_RING="nw,na,nl" (read per call) overrides for sweeps (na, nl
-  // 0: the rule below for that nw).
+  // Ring shape: W slots (hi + lo each), A slots, lo slots.  With W's lo half
+  // pre-split (below) a W slot needs no splitter pass, and what the MMAs wait
+  // on is the lo ring: the RMS warps split A chunk c into a lo slot only once
+  // the MMAs that used that slot finished.  So: A slots = max(4, 2 tiles per
+  // group) (a ring with 3 A slots for 2 tiles per group was seen to stall for
+  // good), 3 W slots when that leaves >= 2 lo slots, the rest to lo (<= 4, <=
+  // A slots).  65,536 x 4096 f32 (tools/tf32_ring.py, bit-identical): rings
+  // (W, A, lo) = (2, 6, 3) 0.567 ms with the in-kernel split; presplit (4, 4,
+  // 1) 0.509, (2, 6, 3) 0.471, (3, 5, 2) 0.428, (3, 4, 3) 0.419 ms.
+  // TIDE_TF32_RING="nw,na,nl" (read per call) overrides for sweeps (na, nl 0:
+  // the rule for that nw).
   const int smem_cap = 227 * 1024;
   const uint32_t misc = 1024 /*w_up*/ + 512 /*bars*/ + 128 /*words*/ + 2048 /*ids*/ + 16;
   auto slots_for = [&](int w) { return (smem_cap - 1024 - w * (int)wslot - (int)misc) / kTfSlot; };
-  auto nl_for = [&](int sl) { return std::min(4, std::max(1, sl / 3)); };
-  int nw = 2, na_req = 0, nl_req = 0;
-  for (int w = kTfMaxNW; w > 2; --w) {
-    const int sl = slots_for(w);
-    if (std::min(kTfMaxNA, sl - nl_for(sl)) >= std::max(4, 2 * tpg)) {
-      nw = w;
-      break;
-    }
-  }
+  int na = std::min(kTfMaxNA, std::max(4, 2 * tpg));
+  auto nl_for = [&](int w) { return std::min(std::min(4, na), slots_for(w) - na); };
+  int nw = nl_for(3) >= 2 ? 3 : 2, na_req = 0, nl_req = 0;
   if (const char* renv = getenv("TIDE_TF32_RING")) {
     int x = 0, y = 0, z = 0;
     if (sscanf(renv, "%d,%d,%d", &x, &y, &z) == 3 && x >= 1 && x <= kTfMaxNW) nw = x, na_req = y, nl_req = z;
   }
   const uint32_t off_a = (uint32_t)nw * wslot;
   const int slots = slots_for(nw);
-  int nl = nl_for(slots);
-  int na = std::min(kTfMaxNA, slots - nl);
+  int nl = nl_for(nw);
   if (na_req > 0 && nl_req > 0 && na_req <= kTfMaxNA && nl_req <= kTfMaxNL && na_req + nl_req <= slots)
     na = na_req, nl = nl_req;
   if (na < 2 || nl < 1) return set_error(TIDE_ERR_UNSUPPORTED, "bottleneck too wide for smem");
@@ -681,6 +704,25 @@ int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
   if ((rc = make_map(&tm_h16, a.h, TIDE_F32, a.d, hrows, a.ld_h, 32, kTfGran))) return rc;
   if ((rc = make_map(&tm_g4, a.h, TIDE_F32, a.d, hrows, a.ld_h, 32, 1))) return rc;
   if ((rc = make_map(&tm_w, a.w_down, TIDE_F32, a.d, a.b, a.d, 32, npad))) return rc;
+  // W's lo half staged in the workspace's upper half (TIDE_TF32_PRESPLIT=0,
+  // read per call, keeps the in-kernel splitter for A/B runs)
+  CUtensorMap tm_wlo = tm_w;
+  float* wlo = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a.workspace) + kWorkspaceScratchOffset);
+  const char* penv = getenv("TIDE_TF32_PRESPLIT");
+  p.w_presplit = 0;
+  if (!(penv && penv[0] == '0') && (size_t)a.b * a.d * 4 <= kWorkspaceScratchBytes &&
+      (reinterpret_cast<uintptr_t>(a.w_down) & 15) == 0 &&
+      make_map(&tm_wlo, wlo, TIDE_F32, a.d, a.b, a.d, 32, npad) == TIDE_OK) {
+    const int64_t n4 = (int64_t)a.b * a.d / 4;
+    int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 4 * 148);
+    // an ordinary launch: it waits for the kernel in flight, which may read
+    // the previous launch's lo half
+    tf32_split_w_kernel<<<blocks, 256, 0, stream>>>(static_cast<const float*>(a.w_down), wlo, n4);
+    if ((rc = check_launch("tf32_split_w_kernel"))) return rc;
+    p.w_presplit = 1;
+    p.inputs_ready = 0;  // the route kernel reads what the split kernel just wrote
+  }
+  cudaGetLastError();
 
   int dev = 0;
   cudaGetDevice(&dev);
@@ -708,7 +750,7 @@ int route_tf32_launch(const RouteArgs& a, cudaStream_t stream) {
     cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
   }
   cfg.attrs = attr;
-  cudaLaunchKernelEx(&cfg, route_tf32_kernel, tm_h128, tm_h64, tm_h32b, tm_h16, tm_w, tm_g4, p);
+  cudaLaunchKernelEx(&cfg, route_tf32_kernel, tm_h128, tm_h64, tm_h32b, tm_h16, tm_w, tm_wlo, tm_g4, p);
   return check_launch("route_tf32_kernel");
 }
 

@@ -455,10 +455,11 @@ def test_repeated_launches_bitwise_identical(pair, monkeypatch):
 @pytest.mark.parametrize("b", [16, 48, 64, 96, 112, 128])
 @pytest.mark.parametrize("n,d", [(20000, 1024), (3000, 4096)])
 def test_f32_tensor_core_ring_shapes_bitwise(n, d, b, monkeypatch):
-    """The 3xTF32 kernel's default ring (up to 4 W slots, route_tf32.cu) and
-    the two-W-slot ring give bit-identical logits, masks and indices (the
-    ring only reorders waits, never arithmetic), over bottleneck widths whose
-    rings differ in every slot count."""
+    """The 3xTF32 kernel's default ring (up to 4 W slots, route_tf32.cu), the
+    two-W-slot ring, and W split in the kernel instead of by the pre-split
+    kernel give bit-identical logits, masks and indices (they reorder waits,
+    never arithmetic), over bottleneck widths whose rings differ in every
+    slot count."""
     need_gpu()
     monkeypatch.setenv("TIDE_F32_TC", "1")
     g = np.random.Generator(np.random.PCG64(n + d + b))
@@ -466,14 +467,16 @@ def test_f32_tensor_core_ring_shapes_bitwise(n, d, b, monkeypatch):
     wu = (g.standard_normal((1, b)) * 0.3).astype(np.float32)
     h = to_dev(g.standard_normal((n, d), dtype=np.float32) * 3.0, "f32")
     outs = []
-    for ring in (None, "2,0,0"):
+    for ring, presplit in ((None, "1"), ("2,0,0", "1"), ("2,0,0", "0")):
+        monkeypatch.setenv("TIDE_TF32_PRESPLIT", presplit)
         if ring:
             monkeypatch.setenv("TIDE_TF32_RING", ring)
         r = P.route(h, _router(wd, wu), theta=0.5, want_logits=True, want_indices=True)
         outs.append({k: r[k].cpu().numpy() for k in ("logits", "mask", "exiting_indices",
                                                        "continuing_indices")})
-    for k in outs[0]:
-        np.testing.assert_array_equal(outs[0][k], outs[1][k], err_msg=k)
+    for o in outs[1:]:
+        for k in outs[0]:
+            np.testing.assert_array_equal(outs[0][k], o[k], err_msg=k)
     if d <= 1024:  # inside the default path's (d, b) range: the 1e-5 contract too
         _, t_ref, m_ref = O.route_logits(h.cpu().numpy(), O.OracleRouter(3, wd, wu))
         check_logits(outs[0]["logits"], t_ref, m_ref, "f32", f"ring b={b}")

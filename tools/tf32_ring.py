@@ -13,7 +13,8 @@ from paper_2603_21365_b200 import _device as D, _native as N  # noqa: E402
 lib = N.load()
 ws = D.workspace().data_ptr()
 s = torch.cuda.current_stream().cuda_stream
-RINGS = [None, "2,0,0"]
+VARIANTS = [("default", {})] + [(f"ring {r}", {"TIDE_TF32_RING": r})
+                               for r in os.environ.get("RINGS", "4,0,0 3,4,3 3,5,2 2,6,3 2,5,4").split()]
 shapes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]] or [(65536, 4096)]
 for shp in shapes:
     n, d = shp[:2]
@@ -24,11 +25,10 @@ for shp in shapes:
     wd = torch.randn((b, d), generator=g, device="cuda") * 0.05
     wu = torch.randn((b,), generator=g, device="cuda") * 0.3
     outs = {}
-    for ring in RINGS:
-        if ring:
-            os.environ["TIDE_TF32_RING"] = ring
-        else:
-            os.environ.pop("TIDE_TF32_RING", None)
+    for ring, env in VARIANTS:
+        for k in ("TIDE_TF32_RING", "TIDE_TF32_PRESPLIT"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
         logits = torch.empty(n, device="cuda")
         mask = torch.empty(n, dtype=torch.uint8, device="cuda")
         ei = torch.empty(n, dtype=torch.int64, device="cuda")
@@ -54,7 +54,7 @@ for shp in shapes:
             best.append(e0.elapsed_time(e1) / 10)
         ne = int(counts[0])
         res = (logits.clone(), mask.clone(), ei[:ne].clone(), ci[: n - ne].clone())
-        if ring is None:
+        if ring == "default":
             outs["ref"] = res
             same = True
         else:
@@ -62,4 +62,4 @@ for shp in shapes:
             same = all(torch.equal(a, b_) for a, b_ in zip(res, r0))
         ms = min(best)
         gbs = (n * d * 4 + b * d * 4) / (ms / 1e3) / 1e9
-        print(f"{n}x{d} b={b} ring={ring or 'default'}: {ms:.4f} ms  {gbs:.0f} GB/s  identical={same}", flush=True)
+        print(f"{n}x{d} b={b} {ring}: {ms:.4f} ms  {gbs:.0f} GB/s  identical={same}", flush=True)

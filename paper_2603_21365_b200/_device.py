@@ -45,8 +45,46 @@ def to_device_f32(x, device=None) -> torch.Tensor:
             t = t.float()
         return t.contiguous()
     arr = np.ascontiguousarray(x, dtype=np.float32)
-    t = torch.from_numpy(arr)
-    return t.to(device or "cuda", non_blocking=False)
+    return upload(arr, device)
+
+
+# Large host arrays go to the device through two pinned staging buffers:
+# the (multi-threaded) host copy of chunk i+1 into one runs while the DMA of
+# chunk i from the other is in flight, instead of torch's pageable copy.
+STAGE_MIN_BYTES = 32 << 20
+STAGE_CHUNK_BYTES = 64 << 20
+_stage_lock = threading.Lock()
+_stages: dict = {}
+
+
+def upload(arr: np.ndarray, device=None) -> torch.Tensor:
+    """C-contiguous host ndarray -> CUDA tensor of the same dtype/shape,
+    ordered on the current stream (the data equals torch.from_numpy(arr).to(dev))."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    src = torch.from_numpy(arr)
+    if arr.nbytes < STAGE_MIN_BYTES or arr.ndim == 0:
+        return src.to(dev)
+    out = torch.empty(src.shape, dtype=src.dtype, device=dev)
+    flat_src, flat_out = src.reshape(-1), out.reshape(-1)
+    step = max(1, STAGE_CHUNK_BYTES // arr.itemsize)
+    stream = torch.cuda.current_stream(dev)
+    with _stage_lock:  # one upload at a time per process uses the staging pair
+        st = _stages.get(dev.index)
+        if st is None:
+            st = [(torch.empty(STAGE_CHUNK_BYTES, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
+                  for _ in range(2)]
+            _stages[dev.index] = st
+        for i, a in enumerate(range(0, flat_src.numel(), step)):
+            buf, ev = st[i % 2]
+            ev.synchronize()  # the DMA that last read this buffer is done
+            m = min(step, flat_src.numel() - a)
+            stage = buf[: m * arr.itemsize].view(src.dtype)
+            stage.copy_(flat_src[a : a + m])
+            flat_out[a : a + m].copy_(stage, non_blocking=True)
+            ev.record(stream)
+    return out
 
 
 def rows_view(t: torch.Tensor):

@@ -101,7 +101,7 @@ def _rows_for(h, router):
         arr = as_f32(h)
         if arr.ndim != 2 or arr.shape[1] != router.hidden_dim:
             raise ValueError(f"expected [batch, {router.hidden_dim}] rows, got {arr.shape}")
-        t = torch.from_numpy(arr).cuda()
+        t = D.upload(arr)
     else:
         t = h
         if t.dim() != 2 or t.shape[1] != router.hidden_dim:
@@ -227,7 +227,7 @@ def batch_compact(h, exit_mask, strategy: str = "auto") -> CompactionResult:
         arr = as_f32(h)
         if arr.ndim != 2:
             raise ValueError(f"expected [batch, d] rows, got {arr.shape}")
-        t = torch.from_numpy(arr).cuda()
+        t = D.upload(arr)
     else:
         t = h
         if t.dim() != 2:
@@ -303,7 +303,7 @@ def _project(exited, gain, eps, positions, out, normalize: bool, what: str) -> N
     if ex_shape[0] == 0 and normalize:
         return
     D.require_cuda()
-    rows = torch.from_numpy(as_f32(exited)).cuda() if ex_host else exited
+    rows = D.upload(as_f32(exited)) if ex_host else exited
     rows, ld = D.rows_view(rows)
     dev = rows.device
     if host_out:

@@ -23,8 +23,8 @@ def batched_cosine_similarity(a, b):
     """ee/tensor_math.py:96-113 on the device: (sims [n] f32, zero_mask [n] bool)."""
     host = D.is_host(a) and D.is_host(b)
     D.require_cuda()
-    ta = torch.from_numpy(as_f32(a)).cuda() if D.is_host(a) else a
-    tb = torch.from_numpy(as_f32(b)).cuda() if D.is_host(b) else b
+    ta = D.upload(as_f32(a)) if D.is_host(a) else a
+    tb = D.upload(as_f32(b)) if D.is_host(b) else b
     if tuple(ta.shape) != tuple(tb.shape) or ta.dim() != 2:
         raise ValueError(f"expected matching [n,d] arrays, got {tuple(ta.shape)} and {tuple(tb.shape)}")
     if ta.dtype != tb.dtype:

@@ -202,3 +202,23 @@ def test_staged_projection_bit_identical(d, dtype, monkeypatch):
     want = np.zeros((2 * n, d), np.float32)
     O.exit_projection(rows.float().cpu().numpy(), gain, 1e-6, pos.cpu().numpy(), want)
     np.testing.assert_array_equal(outs["1"].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("shape,dtype", [((9000, 4099), np.float32), (((33 << 20) // 8 + 5,), np.int64),
+                                         ((70000, 512), np.float32), ((10, 7), np.float32)])
+def test_staged_upload_equals_pageable_copy(shape, dtype):
+    """Host arrays >= 32 MB reach the device through the two pinned staging
+    buffers (_device.upload, chunks of 64 MB, host copy of one chunk under
+    the DMA of the previous): byte-identical to torch's pageable copy, for
+    sizes that are not a multiple of the chunk; two uploads back to back
+    (the second reuses the buffers while the first's DMAs may be in flight)."""
+    need_gpu()
+    Dv = D
+    g = np.random.Generator(np.random.PCG64(sum(shape)))
+    a = (g.standard_normal(shape) * 1000).astype(dtype)
+    b = (g.standard_normal(shape) * 1000).astype(dtype)
+    ta = Dv.upload(a)
+    tb = Dv.upload(b)
+    torch.cuda.synchronize()
+    assert torch.equal(ta.cpu(), torch.from_numpy(a))
+    assert torch.equal(tb.cpu(), torch.from_numpy(b))

@@ -57,6 +57,16 @@ _stage_lock = threading.Lock()
 _stages: dict = {}
 
 
+def _staging(index: int):
+    """The device's pinned staging pair [(buffer, event of its last DMA)] (call under _stage_lock)."""
+    st = _stages.get(index)
+    if st is None:
+        st = [(torch.empty(STAGE_CHUNK_BYTES, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
+              for _ in range(2)]
+        _stages[index] = st
+    return st
+
+
 def upload(arr: np.ndarray, device=None) -> torch.Tensor:
     """C-contiguous host ndarray -> CUDA tensor of the same dtype/shape,
     ordered on the current stream (the data equals torch.from_numpy(arr).to(dev))."""
@@ -71,11 +81,7 @@ def upload(arr: np.ndarray, device=None) -> torch.Tensor:
     step = max(1, STAGE_CHUNK_BYTES // arr.itemsize)
     stream = torch.cuda.current_stream(dev)
     with _stage_lock:  # one upload at a time per process uses the staging pair
-        st = _stages.get(dev.index)
-        if st is None:
-            st = [(torch.empty(STAGE_CHUNK_BYTES, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
-                  for _ in range(2)]
-            _stages[dev.index] = st
+        st = _staging(dev.index)
         for i, a in enumerate(range(0, flat_src.numel(), step)):
             buf, ev = st[i % 2]
             ev.synchronize()  # the DMA that last read this buffer is done
@@ -130,7 +136,42 @@ def ptr(t) -> int:
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
-    return t.detach().cpu().numpy()
+    """CUDA tensor -> host ndarray.  Large results (posthoc logits: 4,096 x
+    50,257 f32 is 823 MB) come back through the pinned staging pair: the DMA
+    of chunk i+1 runs while the host copies chunk i out of the other buffer."""
+    t = t.detach()
+    nbytes = t.numel() * t.element_size()
+    if not t.is_cuda or nbytes < STAGE_MIN_BYTES or t.dtype == torch.bfloat16:
+        return t.cpu().numpy()
+    t = t.contiguous()
+    out = torch.empty(t.shape, dtype=t.dtype)
+    flat_src, flat_out = t.reshape(-1), out.reshape(-1)
+    esz = t.element_size()
+    step = max(1, STAGE_CHUNK_BYTES // esz)
+    dev = t.device
+    stream = torch.cuda.current_stream(dev)
+    with _stage_lock:
+        st = _staging(dev.index)
+        chunks = list(range(0, flat_src.numel(), step))
+
+        def issue(i):
+            buf, ev = st[i % 2]
+            ev.synchronize()  # nothing in flight still reads / writes this buffer
+            a = chunks[i]
+            m = min(step, flat_src.numel() - a)
+            stage = buf[: m * esz].view(t.dtype)
+            stage.copy_(flat_src[a : a + m], non_blocking=True)
+            ev.record(stream)
+            return stage, a, m
+
+        pending = issue(0)
+        for i in range(len(chunks)):
+            stage, a, m = pending
+            if i + 1 < len(chunks):
+                pending = issue(i + 1)
+            st[i % 2][1].synchronize()
+            flat_out[a : a + m].copy_(stage)
+    return out.numpy()
 
 
 class IdentityCache:

@@ -211,7 +211,8 @@ def test_staged_upload_equals_pageable_copy(shape, dtype):
     buffers (_device.upload, chunks of 64 MB, host copy of one chunk under
     the DMA of the previous): byte-identical to torch's pageable copy, for
     sizes that are not a multiple of the chunk; two uploads back to back
-    (the second reuses the buffers while the first's DMAs may be in flight)."""
+    (the second reuses the buffers while the first's DMAs may be in flight),
+    and the staged download (_device.to_host) of large results."""
     need_gpu()
     Dv = D
     g = np.random.Generator(np.random.PCG64(sum(shape)))
@@ -222,3 +223,10 @@ def test_staged_upload_equals_pageable_copy(shape, dtype):
     torch.cuda.synchronize()
     assert torch.equal(ta.cpu(), torch.from_numpy(a))
     assert torch.equal(tb.cpu(), torch.from_numpy(b))
+    # and back: to_host stages large results through the same pair
+    tb.mul_(3)  # produced on the stream right before the download
+    back = Dv.to_host(tb)
+    assert back.dtype == b.dtype and back.shape == b.shape
+    assert np.array_equal(back, (torch.from_numpy(b) * 3).numpy())
+    mask = Dv.to_host(ta.reshape(-1) > 0)
+    assert np.array_equal(mask, a.reshape(-1) > 0)

@@ -230,3 +230,30 @@ def test_staged_upload_equals_pageable_copy(shape, dtype):
     assert np.array_equal(back, (torch.from_numpy(b) * 3).numpy())
     mask = Dv.to_host(ta.reshape(-1) > 0)
     assert np.array_equal(mask, a.reshape(-1) > 0)
+
+
+def test_dropin_host_arrays_through_staging_match_oracle():
+    """The reference-facing calls with host arrays large enough for the
+    staged H2D / D2H (>= 32 MB): fused_layernorm_route's scores equal the
+    device-input call's bitwise (decisions inside the f32 band of the oracle),
+    and batch_compact's host row copies / indices equal the oracle's
+    batch_compact exactly."""
+    need_gpu()
+    g = np.random.Generator(np.random.PCG64(123))
+    n, d = 9000, 1024  # 36.9 MB of f32 rows
+    h = g.standard_normal((n, d), dtype=np.float32)
+    orouter = O.make_router(d, 128, 3, g)
+    router = P.Router(layer=3, w_down=orouter.w_down, w_up=orouter.w_up)
+    s_host = P.fused_layernorm_route(h, router)
+    assert isinstance(s_host, np.ndarray) and s_host.dtype == np.float32
+    s_dev = P.fused_layernorm_route(torch.from_numpy(h).cuda(), router).cpu().numpy()
+    assert np.array_equal(s_host, s_dev)
+    _, t_ref, m_ref = O.route_logits(h[:2048], orouter)
+    assert O.decision_band_ok(s_host[:2048] > np.float32(0.5), t_ref, m_ref, 0.5, 1e-5).all()
+    mask = s_host > np.float32(0.5)
+    got = P.batch_compact(h, mask)
+    want = O.batch_compact(h, mask)
+    for k in ("continuing", "exiting", "continuing_indices", "exiting_indices"):
+        a, b = getattr(got, k), getattr(want, k)
+        assert isinstance(a, np.ndarray), k
+        assert np.array_equal(a, b), k
